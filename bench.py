@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark: effective-batch samples/s of Micro-Batch Streaming on B200.
+
+Default workload (BASELINE.json configs[1]): ResNet-50 @224 (102 classes,
+synthetic Flower-102-shaped uint8 images), mini-batch 1024 streamed as
+micro-batch 128, cross-entropy, SGD(0.01, 0.9, 5e-4), exact_weighted
+normalisation. One STEP = one mini-batch: 8 micro-batch forward/backward
+passes (bf16 autocast on cuDNN, fp32 master weights), 8 fused K1
+normalise+accumulate passes, the loss/grad-norm finalize and one fused K3
+optimizer step.
+
+* ``value``  — inputs already resident in HBM (uint8), staged per micro-batch by K2.
+* ``e2e``    — the same API fed from PINNED HOST memory: every step's micro-batches
+  are copied H2D through the streamer inside the timed region, and every
+  step's loss is read back (D2H).
+* ``no_stream`` — plain torch training at batch = micro (128), data resident: the
+  paper's "w/o MBS" run; ``stream_vs_no_stream`` = value / no_stream.
+* ``roofline`` — K1 (the dominant MBS kernel) achieved algorithmic GB/s, timed
+  live with CUDA events on its stream, vs the measured HBM copy peak.
+* ``cpu_baseline`` — the CPU oracle port (float64 torch-CPU model + NumPy MBS
+  arithmetic, the reference's algorithm) on a bounded sample, rank 0, N=1.
+
+``--impl reference`` runs only that CPU reference path (all host threads).
+Multi-GPU (torchrun): each rank streams its own mini-batch of 1024 (weak
+scaling); the global plan's micro-batches are partitioned across ranks and
+one NCCL all-reduce per mini-batch combines the accumulated gradients.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (the oracle port: the reference's algorithm in float64)
+# ---------------------------------------------------------------------------
+
+def cpu_reference_step(w, model_cpu, st, x, y, n_b, n_mu):
+    from oracle import mbs_oracle as O
+    from oracle.hybrid import TorchGradFn
+    gf = model_cpu
+    params = gf.params()
+    plan = O.plan_split(n_b, n_mu)
+    O.train_mini_batch(gf, params, x, y, plan, w.normalization, st)
+
+
+def run_cpu_reference(w, steps: int, warmup: int, sample_n_b: int, sample_n_mu: int):
+    """Time the float64 CPU oracle on a bounded sample of the workload; returns samples/s."""
+    from oracle import mbs_oracle as O
+    from oracle.hybrid import TorchGradFn
+    from paper_2110_12484_b200.workloads import build_model, synthetic_data
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    torch.manual_seed(0)
+    gf = TorchGradFn(build_model(w), w.loss_kind)
+    st = O.OptState("sgd", 0.01, 0.9, 5e-4) if w.optimizer == "sgd" else O.OptState("adam", 0.01,
+                                                                                       weight_decay=5e-4)
+    acc = O.Accumulator({n: v.shape for n, v in gf.params().items()})
+    x, y = synthetic_data(w, sample_n_b, seed=1)
+    xn = x.double().numpy()
+    yn = y.numpy()
+    plan = O.plan_split(sample_n_b, sample_n_mu)
+    params = gf.params()
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        O.train_mini_batch(gf, params, xn, yn, plan, w.normalization, st, acc)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    sps = sample_n_b * len(times) / sum(times)
+    return sps, threads, float(np.mean(times))
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=16, help="samples per CPU-reference step")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    from paper_2110_12484_b200.workloads import WORKLOADS
+    w = WORKLOADS[args.config]
+    ws, rank, local = _dist()
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        n_mu = max(1, min(w.micro, args.cpu_sample // 2))
+        sps, cores, step_s = run_cpu_reference(w, args.steps, max(1, min(args.warmup, 1)), args.cpu_sample, n_mu)
+        sample = (f"{w.model} {w.sample_shape}: mini-batch {args.cpu_sample} streamed as micro {n_mu}, float64 "
+                  f"torch-CPU model + NumPy MBS arithmetic (oracle port of engine.py/optim.py)")
+        line = {"impl": "reference", "metric": "effective-batch samples/sec", "value": sps, "unit": "samples/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": w.name, "mini": w.mini, "micro": w.micro, "parallelism": "cpu"},
+                "cpu_baseline": {"value": sps, "unit": "samples/s", "cores": cores, "kind": "port",
+                                 "sample": sample},
+                "e2e": {"value": sps, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import paper_2110_12484_b200 as mbs
+    from paper_2110_12484_b200.prof import TIMER
+    from paper_2110_12484_b200.streamer import Staging
+    from paper_2110_12484_b200.workloads import build_model, synthetic_data
+
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    torch.backends.cudnn.benchmark = True
+    torch.manual_seed(1234 + rank)
+
+    model = build_model(w).to(dev).to(memory_format=torch.channels_last)
+    params = mbs.ParameterSet(model)
+    staging = Staging(dtype=torch.bfloat16, channels_last=True)
+    autocast = torch.bfloat16
+    n_b, n_mu = w.mini, w.micro
+    plan = mbs.plan_split(n_b, n_mu)
+
+    # two mini-batches per rank, alternated every step (> L2: each mini-batch is >= 154 MB of uint8)
+    x_dev, y_dev = synthetic_data(w, 2 * n_b, seed=rank, device=dev)
+    x_host, y_host = synthetic_data(w, 2 * n_b, seed=rank)
+    x_host, y_host = x_host.pin_memory(), y_host.pin_memory()
+
+    dp = None
+    if ws > 1:
+        from paper_2110_12484_b200.dp import DataParallelMBS
+        dp = DataParallelMBS(params)
+
+    def make_opt():
+        return mbs.sgd_state(0.01, 0.9, 5e-4) if w.optimizer == "sgd" else mbs.adam_state(0.01, 5e-4)
+
+    acc = mbs.GradientAccumulator(params)
+    st = make_opt()
+    streamer = mbs.make_streamer(x_host, y_host, n_mu, n_slots=3)
+    cs = torch.cuda.current_stream(dev)
+
+    def step(i, host: bool):
+        sl = slice((i % 2) * n_b, (i % 2 + 1) * n_b)
+        x, y = (x_host[sl], y_host[sl]) if host else (x_dev[sl], y_dev[sl])
+        if dp is not None:
+            return dp.train_mini_batch(model, (x, y), n_b, n_mu, w.normalization, w.loss_kind, st, accumulator=acc,
+                                       staging=staging, autocast_dtype=autocast, streamer=streamer if host else None,
+                                       prefetch=True)
+        _, stats = mbs.train_mini_batch(model, params, (x, y), plan, w.normalization, w.loss_kind, st,
+                                        accumulator=acc, staging=staging, autocast_dtype=autocast,
+                                        streamer=streamer if host else None, prefetch=True, keep_outputs=False)
+        return stats
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    def timed(host: bool, steps: int, warmup: int, k1_timer: bool):
+        for i in range(warmup):
+            step(i, host).resolve()
+        barrier()
+        TIMER.reset()
+        TIMER.enabled = k1_timer
+        if host:
+            streamer.timings(flush=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        prev = None
+        losses = []
+        e0.record(cs)
+        for i in range(steps):
+            s = step(i, host)
+            if prev is not None:
+                losses.append(prev.loss)        # D2H read of the previous step's loss (one step behind)
+            prev = s
+        losses.append(prev.loss)
+        e1.record(cs)
+        barrier()
+        TIMER.enabled = False
+        ms = e0.elapsed_time(e1)
+        if ws > 1:
+            t = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, losses
+
+    # --- value: inputs resident in HBM ---
+    with ClockSampler(local) as clocks:
+        ms_dev, _ = timed(False, args.steps, args.warmup, k1_timer=True)
+    kstats = TIMER.summary()
+    launches_value = TIMER.launches
+    samples_total = n_b * args.steps * ws
+    value = samples_total / (ms_dev / 1e3)
+
+    # --- e2e: host-pinned inputs through the streamer ---
+    ms_host, losses = timed(True, args.steps, args.warmup, k1_timer=False)
+    launches_e2e = TIMER.launches
+    e2e = samples_total / (ms_host / 1e3)
+    tim = streamer.timings(flush=True)
+    copy_ms = sum(t[1] for t in tim)
+    blocked_ms = sum(t[2] for t in tim)
+    h2d_bytes = sum(t[3] for t in tim) / max(1, args.steps)
+    overlap = 100.0 * (1.0 - blocked_ms / copy_ms) if copy_ms > 0 else None
+    h2d_gbs = (sum(t[3] for t in tim) / (copy_ms / 1e3) / 1e9) if copy_ms > 0 else None
+    streamer.close()
+
+    # --- no-stream baseline: plain torch training at batch = micro, data resident ---
+    nos = no_stream_baseline(w, dev, n_mu, args.steps, args.warmup, ws)
+
+    k1 = kstats.get("k1_accumulate", {})
+    peak, peak_kind = _peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_k1_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"kernel": "k1_accumulate (mbs_accum_add)", "bound": "hbm", "achieved": k1.get("gbs"),
+                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": (k1.get("gbs") or 0.0) / peak, "traffic": traffic,
+                "algorithmic_bytes_per_launch": k1.get("bytes_per_launch"), "avg_launch_us": (k1.get("avg_ms") or 0) * 1e3,
+                "launches_timed": k1.get("launches"),
+                "bytes_rule": "12 B/param (read g, read acc, write acc); 8 B/param on the first micro-batch "
+                              "(acc = s*g); P = %d" % params.layout.n_params,
+                "other_kernels": {k: {"gbs": v["gbs"], "avg_us": v["avg_ms"] * 1e3, "launches": v["launches"]}
+                                  for k, v in kstats.items() if k != "k1_accumulate"}}
+
+    line = {"metric": "effective-batch samples/sec", "value": value, "unit": "samples/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (uint8 images, random labels; random-init weights)",
+            "config": {"workload": w.name, "model": w.model, "mini_batch_per_gpu": n_b, "micro_batch": n_mu,
+                       "n_micro": plan.n_s_mu, "global_batch": n_b * ws, "parallelism": f"dp{ws}",
+                       "normalization": w.normalization, "optimizer": w.optimizer,
+                       "model_precision": "bf16 autocast on cuDNN/cuBLAS, fp32 master weights; MBS path fp32",
+                       "input": "uint8 NCHW staged to bf16 NHWC by K2",
+                       "l2": "inputs > L2: two alternating mini-batches of %.0f MB" % (x_dev[:n_b].numel() / 1e6)},
+            "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": int(h2d_bytes),
+                    "d2h_bytes_per_step": 8 * (4 + 2 * plan.n_s_mu), "ms_per_step": ms_host / args.steps},
+            "h2d_overlap_pct": overlap, "h2d_gbs": h2d_gbs, "accum_gbs": k1.get("gbs"),
+            "no_stream": nos, "stream_vs_no_stream": value / nos["value"] if nos else None,
+            "e2e_vs_no_stream": e2e / nos["value"] if nos else None,
+            "roofline": roofline, "gpu_launches": launches_value, "gpu_launches_e2e": launches_e2e,
+            "clocks": clocks.summary(), "final_loss": losses[-1] if losses else None}
+
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu_n_b = args.cpu_sample
+        cpu_mu = max(1, cpu_n_b // 2)
+        sps, cores, step_s = run_cpu_reference(w, 1, 1, cpu_n_b, cpu_mu)
+        line["cpu_baseline"] = {"value": sps, "unit": "samples/s", "cores": cores, "kind": "port",
+                                "sample": f"1 mini-batch of {cpu_n_b} as micro {cpu_mu}, {w.model} float64 "
+                                          f"torch-CPU + NumPy MBS oracle, {step_s:.1f} s/step"}
+    if rank == 0:
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def no_stream_baseline(w, dev, batch, steps, warmup, ws):
+    """The paper's 'w/o MBS' run: plain torch training, batch = micro-batch, data resident in HBM."""
+    from paper_2110_12484_b200.losses import compute_loss
+    from paper_2110_12484_b200.workloads import build_model, synthetic_data
+    torch.manual_seed(0)
+    model = build_model(w).to(dev).to(memory_format=torch.channels_last)
+    if w.optimizer == "sgd":
+        opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9, weight_decay=5e-4, fused=True)
+    else:
+        opt = torch.optim.Adam(model.parameters(), lr=0.01, weight_decay=5e-4, fused=True)
+    x, y = synthetic_data(w, 2 * batch, seed=7, device=dev)
+    xs = [x[i * batch:(i + 1) * batch].to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+          for i in range(2)]
+    ys = [y[i * batch:(i + 1) * batch] for i in range(2)]
+
+    def one(i):
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = compute_loss(w.loss_kind, model(xs[i % 2]), ys[i % 2])
+        loss.backward()
+        opt.step()
+        opt.zero_grad(set_to_none=True)
+        return loss
+
+    for i in range(warmup):
+        one(i)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = steps * max(1, w.mini // batch)
+    e0.record()
+    for i in range(n):
+        one(i)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    del model, opt
+    return {"value": batch * n * ws / (ms / 1e3), "unit": "samples/s", "batch": batch,
+            "steps": n, "how": "torch fwd/bwd + fused torch.optim step per batch, bf16 autocast, data in HBM"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,199 @@
+/*
+ * mbs.h — C-ABI of the B200 Micro-Batch Streaming hot path (libmbs_native.so).
+ *
+ * The reference (`/root/reference/pkg/src/mbstream`) is a pure-Python/NumPy
+ * package with no FFI; its "interface" for this path is the functional API in
+ * engine.py / optim.py / tensor.py. Each entry point below names the reference
+ * symbol (file:line) whose semantics it implements. The Python host package
+ * `paper_2110_12484_b200` binds these with ctypes (INTEGRATION.md shows the
+ * binding a reference maintainer would add).
+ *
+ * ABI rules
+ *  - every function is extern "C" and returns an int status (MBS_*); no C++
+ *    exception crosses the boundary;
+ *  - device pointers are BORROWED (owned by the caller, e.g. torch tensors);
+ *    handles own only their scratch (chunk tables, norm partials, stats);
+ *  - `stream` arguments are cudaStream_t passed as void*; every device call is
+ *    stream-ordered and asynchronous unless documented otherwise;
+ *  - one host thread per handle (the reference's threading rule).
+ */
+#ifndef MBS_H
+#define MBS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped to the reference exception types by the shim) ---- */
+#define MBS_OK          0  /* success                                                   */
+#define MBS_EINVAL      1  /* bad argument          -> ValueError                         */
+#define MBS_EOVERFLOW   2  /* too many micro-batches -> AccumulatorOverflowError (engine.py:118-121) */
+#define MBS_EKEY        3  /* key/shape mismatch    -> GradientKeyMismatchError (tensor.py:132-146) */
+#define MBS_ECUDA       4  /* CUDA runtime error    -> RuntimeError                       */
+#define MBS_ENONFINITE  5  /* non-finite gradient   -> NonFiniteError (errors.py:14-19)  */
+
+/* normalization modes, engine.py:34 NORMALIZATION_MODES */
+#define MBS_NORM_PAPER_FAITHFUL 0
+#define MBS_NORM_EXACT_WEIGHTED 1
+#define MBS_NORM_OFF            2
+
+/* element types for staging */
+#define MBS_U8   0
+#define MBS_F32  1
+#define MBS_BF16 2
+#define MBS_F16  3
+#define MBS_F64  4  /* source only (the reference's float64 arrays) */
+
+/* layouts for staging */
+#define MBS_NCHW 0
+#define MBS_NHWC 1
+
+const char* mbs_status_string(int status);
+const char* mbs_last_error(void);         /* last CUDA / argument error text (process-wide) */
+int mbs_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Plan — engine.py:56-78 plan_split, engine.py:81-91 normalization_factor
+ * ------------------------------------------------------------------------- */
+
+/* Writes n_mu (after the n_b < n_mu clamp, engine.py:66-67), n_s_mu
+ * (= ceil(n_b/n_mu), engine.py:68) and, if sizes_out != NULL, up to `cap`
+ * micro-batch sizes (engine.py:69-71). Returns MBS_EINVAL for n_b<1 or n_mu<1
+ * (engine.py:64-65) and when cap < n_s_mu with sizes_out != NULL. */
+int mbs_plan_split(int64_t n_b, int64_t n_mu, int64_t* n_mu_out, int64_t* n_s_mu_out,
+                   int64_t* sizes_out, int64_t cap);
+
+/* engine.py:81-91. MBS_EINVAL for k outside [0, n_s_mu) or unknown mode. */
+int mbs_normalization_factor(int64_t n_b, int64_t n_mu, int64_t k, int mode, double* out);
+
+/* ---------------------------------------------------------------------------
+ * Gradient accumulator — engine.py:100-131 GradientAccumulator (+ accumulate,
+ * engine.py:134-137; the grad norm, tensor.py:126-130). K1.
+ *
+ * The accumulator is a flat fp32 device buffer (borrowed) holding n_segments
+ * parameter segments; segment i lives at seg_offsets[i] (multiple of 4 floats)
+ * with seg_numels[i] elements. begin() is lazy: the first add() after begin()
+ * ASSIGNS acc = s*g (no zero pass, no acc read); later adds do acc += s*g.
+ * ------------------------------------------------------------------------- */
+typedef struct mbs_accum* mbs_accum_t;
+
+int mbs_accum_create(float* acc_dev, int64_t acc_numel, int64_t n_segments,
+                     const int64_t* seg_offsets, const int64_t* seg_numels,
+                     int64_t max_micro, mbs_accum_t* out);
+int mbs_accum_destroy(mbs_accum_t h);
+/* engine.py:110-115 begin(expected); expected < 0 means "no limit". */
+int mbs_accum_begin(mbs_accum_t h, int64_t expected);
+/* Materialise the pending zero of begin() (only needed when the sums are read
+ * before any add()). */
+int mbs_accum_zero(mbs_accum_t h, void* stream);
+/* engine.py:117-128 add(grads) with the normalisation factor fused (the
+ * reference folds it into the backward seed, engine.py:214-215, which is the
+ * same linear map). `grads[i]` is the device gradient of segment
+ * seg_begin+i (dense, same element order as the parameter). `loss_dev`
+ * (nullable) is this micro-batch's raw mean loss, recorded for the stats
+ * (engine.py:217-218) with its normalisation factor `loss_factor` (which
+ * equals `factor` unless the caller already applied it in the backward seed)
+ * and `loss_weight` = its sample count size_k (the weight of engine.py:221). `last` != 0 additionally emits per-chunk
+ * ||acc||^2 partials for the grad norm. Returns MBS_EOVERFLOW past
+ * `expected`. */
+int mbs_accum_add(mbs_accum_t h, const float* const* grads, int64_t seg_begin,
+                  int64_t seg_count, double factor, const float* loss_dev,
+                  double loss_factor, double loss_weight, int last, void* stream);
+/* Same, over a flat gradient buffer laid out exactly like acc. */
+int mbs_accum_add_flat(mbs_accum_t h, const float* g_flat, double factor,
+                       const float* loss_dev, double loss_factor, double loss_weight, int last,
+                       void* stream);
+/* Recompute the ||acc||^2 partials over the whole buffer (used after an
+ * all-reduce in data-parallel mode). */
+int mbs_accum_norm(mbs_accum_t h, void* stream);
+/* Reduce the partials and the loss record: writes to device `stats_dev`
+ * (double[4 + 2*max_micro]): [0]=||acc||^2, [1]=mini-batch loss
+ * sum_k size_k*loss_k/n_b (engine.py:221, sequential in plan order),
+ * [2]=non-finite flag, [3]=#micro, [4..4+n)=raw losses,
+ * [4+max_micro..)=normalised losses (raw*factor, engine.py:218).
+ * Deterministic (fixed reduction order). */
+int mbs_accum_finalize(mbs_accum_t h, int64_t n_b, double* stats_dev, void* stream);
+int mbs_accum_seen(mbs_accum_t h, int64_t* seen, int64_t* expected);
+
+/* ---------------------------------------------------------------------------
+ * Optimizer step over flat buffers — optim.py:52-65 sgd_step, optim.py:68-93
+ * adam_step (coupled weight decay). K3. `guard_dev` (nullable) points at a
+ * double; when it is non-finite the step is skipped on device (params stay
+ * intact, the host raises NonFiniteError when it reads the stats).
+ * `velocity`/`m`/`v` are device fp32 buffers of `numel` elements, zero at
+ * step 0 (the reference creates them lazily as zeros, optim.py:58-61,78-83).
+ * ------------------------------------------------------------------------- */
+int mbs_sgd_step(float* w, const float* grad, float* velocity, int64_t numel, double lr,
+                 double momentum, double weight_decay, const double* guard_dev, void* stream);
+int mbs_adam_step(float* w, const float* grad, float* m, float* v, int64_t numel, double lr,
+                  double beta1, double beta2, double eps, double weight_decay,
+                  int64_t step /* t = step_count + 1 */, const double* guard_dev, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Staging — engine.py:310-311 (x[order[mini]]) + engine.py:149-151
+ * (ascontiguousarray(x[lo:hi])) + tensor.py:20-22 (dtype coercion). K2.
+ *
+ * dst row r := cast(src row (rows ? rows[r] : row0 + r)); each row is a
+ * C x H x W sample stored NCHW in `src`; dst is NCHW or NHWC in dst_dtype.
+ * Casts are exact (u8->f32/bf16/f16) or IEEE round-to-nearest-even
+ * (f32/f64->f32/bf16/f16), bit-identical to torch's .to(dtype) (f64->bf16
+ * rounds through f32 exactly like torch does). `src` may be device
+ * memory or pinned/registered host memory (zero-copy). `rows` is a DEVICE
+ * array (nullable).
+ * ------------------------------------------------------------------------- */
+int mbs_stage(const void* src, int src_dtype, const int64_t* rows, int64_t row0, int64_t n_rows,
+              int64_t C, int64_t H, int64_t W, void* dst, int dst_dtype, int dst_layout,
+              void* stream);
+/* Byte-exact row gather (targets, masks, labels): dst[r] = src[rows? rows[r] : row0+r]. */
+int mbs_gather_rows(const void* src, const int64_t* rows, int64_t row0, int64_t n_rows,
+                    int64_t row_bytes, void* dst, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Host->device micro-batch streamer — engine.py:140-163 _micro_batches
+ * (prefetch worker, two slots) re-designed as a pinned ring of `n_slots`
+ * slots, a native gather thread pool and cudaMemcpyAsync on a copy stream.
+ *
+ * A job gathers `n_rows` rows (rows[] host indices, or row0.. contiguous) of
+ * up to MBS_MAX_PARTS host tensors into pinned slot `slot`, then copies each
+ * part to its device destination on `copy_stream` and records the slot's
+ * "ready" event. When a part's host source is already pinned and the rows are
+ * contiguous, the gather is skipped and the copy reads the source directly.
+ * mbs_streamer_wait() makes `compute_stream` wait for the slot (host blocks
+ * only until the job has been issued, never for the copy itself);
+ * mbs_streamer_release() records that compute finished reading the slot's
+ * device buffers so the next copy into them is ordered after it.
+ * ------------------------------------------------------------------------- */
+#define MBS_MAX_PARTS 4
+typedef struct mbs_streamer* mbs_streamer_t;
+typedef struct {
+    const void* src;        /* host base pointer of the dataset tensor        */
+    int64_t row_bytes;      /* bytes per sample                                */
+    void* dst;              /* device destination (n_rows * row_bytes)         */
+    int src_pinned;         /* src is page-locked (skip gather when contiguous)*/
+} mbs_part_t;
+
+int mbs_streamer_create(int n_slots, int64_t slot_bytes, int n_threads, void* copy_stream,
+                        mbs_streamer_t* out);
+int mbs_streamer_destroy(mbs_streamer_t h);
+/* `job_out` (nullable) receives the job's sequence number for mbs_streamer_timing. */
+int mbs_streamer_submit(mbs_streamer_t h, int slot, const mbs_part_t* parts, int n_parts,
+                        const int64_t* rows, int64_t row0, int64_t n_rows, int64_t* job_out);
+int mbs_streamer_wait(mbs_streamer_t h, int slot, void* compute_stream);
+int mbs_streamer_release(mbs_streamer_t h, int slot, void* compute_stream);
+/* Timing of job `job` (ms): host gather time, device copy time (copy-stream
+ * events) and the time compute was blocked waiting for it
+ * (max(0, copy_end - compute_reached_wait)); bytes copied. Synchronises on the
+ * job's events; records are kept for the last 256 jobs. */
+int mbs_streamer_timing(mbs_streamer_t h, int64_t job, double* gather_ms, double* copy_ms,
+                        double* blocked_ms, int64_t* bytes);
+/* Multi-threaded host gather into a caller buffer (used by tests and the
+ * epoch driver): dst[r] = src[rows[r]] for row_bytes-sized rows. */
+int mbs_host_gather(const void* src, int64_t row_bytes, const int64_t* rows, int64_t n_rows,
+                    void* dst, int n_threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MBS_H */

@@ -1,0 +1,547 @@
+// K1 (fused normalise + accumulate + grad-norm partials), the loss-stat /
+// grad-norm finalize, and K3 (fused SGD-momentum / Adam step) for sm_100a.
+//
+// Reference semantics:
+//   GradientAccumulator.begin/add      engine.py:110-128 (sums[name] += grad, plan order)
+//   factor folded into backward seed   engine.py:210-215, nn.py:596 (linear in the seed)
+//   mini-batch loss / stats            engine.py:217-221
+//   GradientSet.l2_norm                tensor.py:126-130
+//   sgd_step / adam_step               optim.py:52-65 / optim.py:68-93
+//
+// All kernels are HBM-bound streaming passes: 128-bit loads/stores, a few
+// independent float4s in flight per thread, one CTA per 8192-element chunk
+// (the hardware block scheduler balances the tail), no atomics, and a fixed
+// reduction order so the grad norm is bit-reproducible run to run.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "mbs_common.h"
+
+namespace mbs {
+
+static std::mutex g_err_mu;
+static std::string g_last_error;  // process-wide: the streamer's worker thread reports here too
+void set_error(const std::string& msg) {
+    std::lock_guard<std::mutex> g(g_err_mu);
+    g_last_error = msg;
+}
+
+constexpr int kThreads = 256;
+constexpr int kChunk = 8192;       // elements per CTA work unit (K1 / norm)
+constexpr int kMaxPtrs = 1024;     // gradient pointers per K1 launch (kernel-param table)
+constexpr int kUnroll = 4;
+
+struct Chunk {
+    int64_t acc_off;   // element offset into acc
+    int64_t g_off;     // element offset into the segment's gradient tensor
+    int32_t seg;       // segment index
+    int32_t len;       // elements in this chunk (<= kChunk)
+};
+
+struct GradPtrs {
+    const float* p[kMaxPtrs];
+};
+
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ double sq4(float4 a) {
+    double x = a.x, y = a.y, z = a.z, w = a.w;
+    return x * x + y * y + z * z + w * w;
+}
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* smem) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) smem[warp] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) r += smem[i];
+    }
+    return r;  // valid in thread 0 only
+}
+
+// K1: acc[c] = s*g (ASSIGN) or acc[c] += s*g, per chunk; optional ||acc||^2 partial per chunk.
+template <bool ASSIGN, bool NORM>
+__global__ void __launch_bounds__(kThreads)
+k_accum(float* __restrict__ acc, const Chunk* __restrict__ chunks, int64_t chunk0, int seg0,
+        const __grid_constant__ GradPtrs gp, float s, double* __restrict__ partials,
+        const float* __restrict__ loss, double* __restrict__ loss_slot,
+        double* __restrict__ factor_slot, double factor, double* __restrict__ weight_slot, double weight) {
+    __shared__ double red[kThreads / 32];
+    const Chunk c = chunks[chunk0 + blockIdx.x];
+    const float* __restrict__ g = gp.p[c.seg - seg0] + c.g_off;
+    float* __restrict__ a = acc + c.acc_off;
+    double sq = 0.0;
+    int done = 0;
+    if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+        const int n4 = c.len >> 2;
+        const float4* g4 = reinterpret_cast<const float4*>(g);
+        float4* a4 = reinterpret_cast<float4*>(a);
+        for (int base = threadIdx.x; base < n4; base += kThreads * kUnroll) {
+            float4 gv[kUnroll], av[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int i = base + u * kThreads;
+                if (i < n4) {
+                    gv[u] = ld_stream(g4 + i);
+                    if (!ASSIGN) av[u] = a4[i];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int i = base + u * kThreads;
+                if (i < n4) {
+                    float4 r;
+                    if (ASSIGN) {
+                        r.x = s * gv[u].x; r.y = s * gv[u].y; r.z = s * gv[u].z; r.w = s * gv[u].w;
+                    } else {
+                        r.x = fmaf(s, gv[u].x, av[u].x); r.y = fmaf(s, gv[u].y, av[u].y);
+                        r.z = fmaf(s, gv[u].z, av[u].z); r.w = fmaf(s, gv[u].w, av[u].w);
+                    }
+                    a4[i] = r;
+                    if (NORM) sq += sq4(r);
+                }
+            }
+        }
+        done = n4 << 2;
+    }
+    for (int i = done + threadIdx.x; i < c.len; i += kThreads) {  // tail / unaligned gradient
+        const float r = ASSIGN ? s * g[i] : fmaf(s, g[i], a[i]);
+        a[i] = r;
+        if (NORM) sq += (double)r * (double)r;
+    }
+    if (NORM) {
+        const double t = block_sum<kThreads>(sq, red);
+        if (threadIdx.x == 0) partials[chunk0 + blockIdx.x] = t;
+    }
+    if (loss != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+        *loss_slot = (double)*loss;
+        *factor_slot = factor;
+        *weight_slot = weight;
+    }
+}
+
+// ||acc||^2 partials per chunk (post-all-reduce norm).
+__global__ void __launch_bounds__(kThreads)
+k_sumsq(const float* __restrict__ acc, const Chunk* __restrict__ chunks, double* __restrict__ partials) {
+    __shared__ double red[kThreads / 32];
+    const Chunk c = chunks[blockIdx.x];
+    const float* a = acc + c.acc_off;
+    double sq = 0.0;
+    const int n4 = c.len >> 2;
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    for (int i = threadIdx.x; i < n4; i += kThreads) sq += sq4(ld_stream(a4 + i));
+    for (int i = (n4 << 2) + threadIdx.x; i < c.len; i += kThreads) sq += (double)a[i] * (double)a[i];
+    const double t = block_sum<kThreads>(sq, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = t;
+}
+
+// Finalize: deterministic reduction of the norm partials + the loss record (engine.py:217-221).
+__global__ void __launch_bounds__(1024)
+k_finalize(const double* __restrict__ partials, int64_t n_partials,
+           const double* __restrict__ losses, const double* __restrict__ factors,
+           const double* __restrict__ weights, int64_t n_micro, int64_t max_micro, int64_t n_b,
+           double* __restrict__ stats) {
+    __shared__ double red[32];
+    double v = 0.0;
+    for (int64_t i = threadIdx.x; i < n_partials; i += blockDim.x) v += partials[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double norm2 = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) norm2 += red[i];
+        // mini-batch loss: sequential sum over micro-batches in plan order (engine.py:221)
+        double lsum = 0.0;
+        for (int64_t j = 0; j < n_micro; ++j) lsum += weights[j] * losses[j];
+        stats[0] = norm2;
+        stats[1] = lsum / (double)n_b;
+        stats[2] = isfinite(norm2) ? 0.0 : 1.0;
+        stats[3] = (double)n_micro;
+        for (int64_t j = 0; j < n_micro; ++j) {
+            stats[4 + j] = losses[j];
+            stats[4 + max_micro + j] = losses[j] * factors[j];
+        }
+    }
+}
+
+__device__ __forceinline__ bool guard_tripped(const double* guard) {
+    return guard != nullptr && !isfinite(*guard);
+}
+
+// K3a: optim.py:52-65 — g' = g + wd*w; v = mu*v + g'; w -= lr*v.
+template <bool READ_V, bool WD>
+__global__ void __launch_bounds__(kThreads)
+k_sgd(float4* __restrict__ w, const float4* __restrict__ g, float4* __restrict__ v, int64_t n4,
+      float lr, float mu, float wd, const double* __restrict__ guard) {
+    if (guard_tripped(guard)) return;
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n4; i += stride) {
+        const float4 gg = ld_stream(g + i);
+        float4 ww = w[i];
+        float4 vv = READ_V ? v[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float gx = WD ? fmaf(wd, ww.x, gg.x) : gg.x;
+        float gy = WD ? fmaf(wd, ww.y, gg.y) : gg.y;
+        float gz = WD ? fmaf(wd, ww.z, gg.z) : gg.z;
+        float gw = WD ? fmaf(wd, ww.w, gg.w) : gg.w;
+        vv.x = fmaf(mu, vv.x, gx); vv.y = fmaf(mu, vv.y, gy);
+        vv.z = fmaf(mu, vv.z, gz); vv.w = fmaf(mu, vv.w, gw);
+        ww.x = fmaf(-lr, vv.x, ww.x); ww.y = fmaf(-lr, vv.y, ww.y);
+        ww.z = fmaf(-lr, vv.z, ww.z); ww.w = fmaf(-lr, vv.w, ww.w);
+        v[i] = vv;
+        w[i] = ww;
+    }
+}
+
+__device__ __forceinline__ void adam1(float& w, float& m, float& v, float g, float lr, float b1,
+                                      float omb1, float b2, float omb2, float c1, float c2,
+                                      float eps, float wd) {
+    if (wd != 0.f) g = fmaf(wd, w, g);
+    m = fmaf(b1, m, omb1 * g);
+    v = fmaf(b2, v, omb2 * g * g);
+    const float mh = __fdiv_rn(m, c1);
+    const float vh = __fsqrt_rn(__fdiv_rn(v, c2));
+    w = w - __fdiv_rn(lr * mh, vh + eps);
+}
+
+// K3b: optim.py:68-93 — bias-corrected Adam, coupled weight decay.
+__global__ void __launch_bounds__(kThreads)
+k_adam(float4* __restrict__ w, const float4* __restrict__ g, float4* __restrict__ m,
+       float4* __restrict__ v, int64_t n4, float lr, float b1, float b2, float c1, float c2,
+       float eps, float wd, const double* __restrict__ guard) {
+    if (guard_tripped(guard)) return;
+    const float omb1 = 1.f - b1, omb2 = 1.f - b2;
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n4; i += stride) {
+        const float4 gg = ld_stream(g + i);
+        float4 ww = w[i], mm = m[i], vv = v[i];
+        adam1(ww.x, mm.x, vv.x, gg.x, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
+        adam1(ww.y, mm.y, vv.y, gg.y, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
+        adam1(ww.z, mm.z, vv.z, gg.z, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
+        adam1(ww.w, mm.w, vv.w, gg.w, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
+        w[i] = ww; m[i] = mm; v[i] = vv;
+    }
+}
+
+static int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
+static int stream_grid(int64_t n4) {
+    const int64_t want = (n4 + kThreads - 1) / kThreads;
+    const int64_t cap = (int64_t)sm_count() * (2048 / kThreads) * 2;  // two full waves, grid-stride
+    return (int)std::max<int64_t>(1, std::min(want, cap));
+}
+
+}  // namespace mbs
+
+using namespace mbs;
+
+struct mbs_accum {
+    float* acc = nullptr;
+    int64_t numel = 0;
+    std::vector<int64_t> off, num;
+    std::vector<int64_t> seg_chunk0;   // first chunk of each segment (size nseg+1)
+    Chunk* d_chunks = nullptr;
+    int64_t n_chunks = 0;
+    double* d_partials = nullptr;
+    double* d_losses = nullptr;        // [max_micro] raw loss per local micro-batch
+    double* d_factors = nullptr;       // [max_micro]
+    double* d_weights = nullptr;       // [max_micro] sample count of each micro-batch
+    int64_t max_micro = 0;
+    int64_t expected = -1;
+    int64_t seen = 0;
+    bool fresh = true;                 // begin() pending: next add assigns
+    int64_t covered = 0;               // segments added so far for the current micro-batch
+};
+
+extern "C" {
+
+const char* mbs_status_string(int s) {
+    switch (s) {
+        case MBS_OK: return "ok";
+        case MBS_EINVAL: return "invalid argument";
+        case MBS_EOVERFLOW: return "accumulator overflow";
+        case MBS_EKEY: return "gradient key/shape mismatch";
+        case MBS_ECUDA: return "CUDA error";
+        case MBS_ENONFINITE: return "non-finite values";
+        default: return "unknown status";
+    }
+}
+
+const char* mbs_last_error(void) {
+    static thread_local std::string copy;
+    std::lock_guard<std::mutex> g(g_err_mu);
+    copy = g_last_error;
+    return copy.c_str();
+}
+
+int mbs_version(void) { return 1; }
+
+int mbs_plan_split(int64_t n_b, int64_t n_mu, int64_t* n_mu_out, int64_t* n_s_mu_out,
+                   int64_t* sizes_out, int64_t cap) {
+    if (n_b < 1 || n_mu < 1)
+        return invalid("batch sizes must be positive, got n_b=" + std::to_string(n_b) +
+                       ", n_mu=" + std::to_string(n_mu));
+    if (n_b < n_mu) n_mu = n_b;                       // engine.py:66-67
+    const int64_t q = n_b / n_mu, r = n_b % n_mu;
+    const int64_t n_s_mu = q + (r ? 1 : 0);           // ceil, engine.py:68
+    if (n_mu_out) *n_mu_out = n_mu;
+    if (n_s_mu_out) *n_s_mu_out = n_s_mu;
+    if (sizes_out) {
+        if (cap < n_s_mu) return invalid("sizes_out capacity smaller than n_s_mu");
+        for (int64_t i = 0; i < q; ++i) sizes_out[i] = n_mu;   // engine.py:69
+        if (r) sizes_out[q] = r;                               // engine.py:70-71
+    }
+    return MBS_OK;
+}
+
+int mbs_normalization_factor(int64_t n_b, int64_t n_mu, int64_t k, int mode, double* out) {
+    int64_t nm = 0, ns = 0;
+    int st = mbs_plan_split(n_b, n_mu, &nm, &ns, nullptr, 0);
+    if (st) return st;
+    if (k < 0 || k >= ns)
+        return invalid("micro-batch index " + std::to_string(k) + " outside plan of " + std::to_string(ns));
+    const int64_t size_k = (k == ns - 1 && n_b % nm) ? n_b % nm : nm;
+    switch (mode) {
+        case MBS_NORM_PAPER_FAITHFUL: *out = 1.0 / (double)ns; return MBS_OK;          // engine.py:85-86
+        case MBS_NORM_EXACT_WEIGHTED: *out = (double)size_k / (double)n_b; return MBS_OK;  // 87-88
+        case MBS_NORM_OFF: *out = 1.0; return MBS_OK;                                   // 89-90
+        default: return invalid("unknown normalization mode " + std::to_string(mode));
+    }
+}
+
+int mbs_accum_create(float* acc_dev, int64_t acc_numel, int64_t n_segments,
+                     const int64_t* seg_offsets, const int64_t* seg_numels, int64_t max_micro,
+                     mbs_accum_t* out) {
+    if (!out || !acc_dev || acc_numel <= 0 || n_segments <= 0 || !seg_offsets || !seg_numels || max_micro < 1)
+        return invalid("mbs_accum_create: bad arguments");
+    if ((reinterpret_cast<uintptr_t>(acc_dev) & 15) != 0) return invalid("accumulator must be 16-byte aligned");
+    auto* h = new mbs_accum();
+    h->acc = acc_dev;
+    h->numel = acc_numel;
+    h->max_micro = max_micro;
+    std::vector<Chunk> chunks;
+    int64_t prev_end = 0;
+    for (int64_t i = 0; i < n_segments; ++i) {
+        const int64_t o = seg_offsets[i], n = seg_numels[i];
+        if (o % 4 != 0 || n < 0 || o < prev_end || o + n > acc_numel) {
+            delete h;
+            return invalid("segment " + std::to_string(i) + " misaligned, overlapping or out of range");
+        }
+        prev_end = o + n;
+        h->off.push_back(o);
+        h->num.push_back(n);
+        h->seg_chunk0.push_back((int64_t)chunks.size());
+        for (int64_t s = 0; s < n; s += kChunk) {
+            Chunk c;
+            c.acc_off = o + s;
+            c.g_off = s;
+            c.seg = (int32_t)i;
+            c.len = (int32_t)std::min<int64_t>(kChunk, n - s);
+            chunks.push_back(c);
+        }
+    }
+    h->seg_chunk0.push_back((int64_t)chunks.size());
+    h->n_chunks = (int64_t)chunks.size();
+    cudaError_t e = cudaMalloc(&h->d_chunks, sizeof(Chunk) * std::max<int64_t>(1, h->n_chunks));
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_chunks, chunks.data(), sizeof(Chunk) * h->n_chunks, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&h->d_partials, sizeof(double) * std::max<int64_t>(1, h->n_chunks));
+    if (e == cudaSuccess) e = cudaMemset(h->d_partials, 0, sizeof(double) * std::max<int64_t>(1, h->n_chunks));
+    if (e == cudaSuccess) e = cudaMalloc(&h->d_losses, sizeof(double) * max_micro * 3);
+    if (e == cudaSuccess) e = cudaMemset(h->d_losses, 0, sizeof(double) * max_micro * 3);
+    if (e != cudaSuccess) {
+        mbs_accum_destroy(h);
+        return cuda_status(e, "mbs_accum_create");
+    }
+    h->d_factors = h->d_losses + max_micro;
+    h->d_weights = h->d_losses + 2 * max_micro;
+    *out = h;
+    return MBS_OK;
+}
+
+int mbs_accum_destroy(mbs_accum_t h) {
+    if (!h) return MBS_OK;
+    if (h->d_chunks) cudaFree(h->d_chunks);
+    if (h->d_partials) cudaFree(h->d_partials);
+    if (h->d_losses) cudaFree(h->d_losses);
+    delete h;
+    return MBS_OK;
+}
+
+int mbs_accum_begin(mbs_accum_t h, int64_t expected) {
+    if (!h) return invalid("null accumulator");
+    if (expected > h->max_micro) return invalid("expected micro-batches exceed the handle's max_micro");
+    h->expected = expected;
+    h->seen = 0;
+    h->covered = 0;
+    h->fresh = true;
+    return MBS_OK;
+}
+
+int mbs_accum_zero(mbs_accum_t h, void* stream) {
+    if (!h) return invalid("null accumulator");
+    MBS_CK(cudaMemsetAsync(h->acc, 0, sizeof(float) * h->numel, (cudaStream_t)stream));
+    h->fresh = false;
+    return MBS_OK;
+}
+
+int mbs_accum_seen(mbs_accum_t h, int64_t* seen, int64_t* expected) {
+    if (!h) return invalid("null accumulator");
+    if (seen) *seen = h->seen;
+    if (expected) *expected = h->expected;
+    return MBS_OK;
+}
+
+static int launch_accum(mbs_accum_t h, const float* const* grads, int64_t seg_begin, int64_t seg_count,
+                        float s, const float* loss_dev, double factor, double weight, bool assign, bool norm,
+                        cudaStream_t st) {
+    const int64_t slot = h->seen;
+    for (int64_t b = 0; b < seg_count; b += kMaxPtrs) {
+        const int64_t cnt = std::min<int64_t>(kMaxPtrs, seg_count - b);
+        GradPtrs gp;
+        for (int64_t i = 0; i < cnt; ++i) gp.p[i] = grads[b + i];
+        const int64_t s0 = seg_begin + b;
+        const int64_t c0 = h->seg_chunk0[s0], c1 = h->seg_chunk0[s0 + cnt];
+        if (c1 == c0) continue;
+        const float* lp = (b == 0) ? loss_dev : nullptr;
+        dim3 grid((unsigned)(c1 - c0));
+        if (assign && norm)
+            k_accum<true, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_chunks, c0, (int)s0, gp, s, h->d_partials, lp, h->d_losses + slot, h->d_factors + slot, factor, h->d_weights + slot, weight);
+        else if (assign)
+            k_accum<true, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_chunks, c0, (int)s0, gp, s, h->d_partials, lp, h->d_losses + slot, h->d_factors + slot, factor, h->d_weights + slot, weight);
+        else if (norm)
+            k_accum<false, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_chunks, c0, (int)s0, gp, s, h->d_partials, lp, h->d_losses + slot, h->d_factors + slot, factor, h->d_weights + slot, weight);
+        else
+            k_accum<false, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_chunks, c0, (int)s0, gp, s, h->d_partials, lp, h->d_losses + slot, h->d_factors + slot, factor, h->d_weights + slot, weight);
+        MBS_CK_LAUNCH("k_accum");
+    }
+    return MBS_OK;
+}
+
+int mbs_accum_add(mbs_accum_t h, const float* const* grads, int64_t seg_begin, int64_t seg_count,
+                  double factor, const float* loss_dev, double loss_factor, double loss_weight, int last,
+                  void* stream) {
+    if (!h || !grads) return invalid("null accumulator or gradient table");
+    const int64_t nseg = (int64_t)h->off.size();
+    if (seg_begin < 0 || seg_count < 1 || seg_begin + seg_count > nseg)
+        return invalid("segment range out of bounds");
+    // A micro-batch may arrive as several calls (gradient buckets issued during
+    // the last backward, any order); it is complete once every segment has been
+    // added. The overflow guard (engine.py:118-121) runs on its first call.
+    if (h->covered == 0) {
+        if (h->expected >= 0 && h->seen >= h->expected) {
+            set_error("already accumulated " + std::to_string(h->seen) + " of " +
+                      std::to_string(h->expected) + " micro-batches");
+            return MBS_EOVERFLOW;
+        }
+        if (h->seen >= h->max_micro) {
+            set_error("micro-batch count exceeds the handle's max_micro");
+            return MBS_EOVERFLOW;
+        }
+    }
+    if (h->covered + seg_count > nseg) {
+        set_error("gradient segments exceed the accumulator's parameter set");
+        return MBS_EKEY;
+    }
+    for (int64_t i = 0; i < seg_count; ++i)
+        if (!grads[i] && h->num[seg_begin + i] > 0) {
+            set_error("missing gradient for segment " + std::to_string(seg_begin + i));
+            return MBS_EKEY;
+        }
+    int st = launch_accum(h, grads, seg_begin, seg_count, (float)factor, loss_dev, loss_factor, loss_weight, h->fresh,
+                          last != 0, (cudaStream_t)stream);
+    if (st) return st;
+    h->covered += seg_count;
+    if (h->covered == nseg) {
+        h->covered = 0;
+        h->seen += 1;
+        h->fresh = false;
+    }
+    return MBS_OK;
+}
+
+int mbs_accum_add_flat(mbs_accum_t h, const float* g_flat, double factor, const float* loss_dev,
+                       double loss_factor, double loss_weight, int last, void* stream) {
+    if (!h || !g_flat) return invalid("null accumulator or gradient");
+    std::vector<const float*> ptrs(h->off.size());
+    for (size_t i = 0; i < ptrs.size(); ++i) ptrs[i] = g_flat + h->off[i];
+    return mbs_accum_add(h, ptrs.data(), 0, (int64_t)ptrs.size(), factor, loss_dev, loss_factor, loss_weight, last,
+                         stream);
+}
+
+int mbs_accum_norm(mbs_accum_t h, void* stream) {
+    if (!h) return invalid("null accumulator");
+    if (h->n_chunks == 0) return MBS_OK;
+    k_sumsq<<<(unsigned)h->n_chunks, kThreads, 0, (cudaStream_t)stream>>>(h->acc, h->d_chunks, h->d_partials);
+    MBS_CK_LAUNCH("k_sumsq");
+    return MBS_OK;
+}
+
+int mbs_accum_finalize(mbs_accum_t h, int64_t n_b, double* stats_dev, void* stream) {
+    if (!h || !stats_dev || n_b < 1) return invalid("mbs_accum_finalize: null handle/stats or n_b < 1");
+    k_finalize<<<1, 1024, 0, (cudaStream_t)stream>>>(h->d_partials, h->n_chunks, h->d_losses, h->d_factors,
+                                                    h->d_weights, h->seen, h->max_micro, n_b, stats_dev);
+    MBS_CK_LAUNCH("k_finalize");
+    return MBS_OK;
+}
+
+int mbs_sgd_step(float* w, const float* grad, float* velocity, int64_t numel, double lr, double momentum,
+                 double weight_decay, const double* guard_dev, void* stream) {
+    if (!w || !grad || !velocity || numel <= 0 || numel % 4)
+        return invalid("mbs_sgd_step: null buffer or numel not a positive multiple of 4");
+    if (((uintptr_t)w | (uintptr_t)grad | (uintptr_t)velocity) & 15) return invalid("mbs_sgd_step: buffers must be 16-byte aligned");
+    const int64_t n4 = numel / 4;
+    const int grid = stream_grid(n4);
+    auto st = (cudaStream_t)stream;
+    auto W = reinterpret_cast<float4*>(w);
+    auto G = reinterpret_cast<const float4*>(grad);
+    auto V = reinterpret_cast<float4*>(velocity);
+    const bool rv = momentum != 0.0, wd = weight_decay != 0.0;
+    if (rv && wd) k_sgd<true, true><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, (float)momentum, (float)weight_decay, guard_dev);
+    else if (rv) k_sgd<true, false><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, (float)momentum, 0.f, guard_dev);
+    else if (wd) k_sgd<false, true><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, 0.f, (float)weight_decay, guard_dev);
+    else k_sgd<false, false><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, 0.f, 0.f, guard_dev);
+    MBS_CK_LAUNCH("k_sgd");
+    return MBS_OK;
+}
+
+int mbs_adam_step(float* w, const float* grad, float* m, float* v, int64_t numel, double lr, double beta1,
+                  double beta2, double eps, double weight_decay, int64_t step, const double* guard_dev,
+                  void* stream) {
+    if (!w || !grad || !m || !v || numel <= 0 || numel % 4 || step < 1)
+        return invalid("mbs_adam_step: null buffer, numel not a positive multiple of 4, or step < 1");
+    if (((uintptr_t)w | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v) & 15) return invalid("mbs_adam_step: buffers must be 16-byte aligned");
+    const double c1 = 1.0 - pow(beta1, (double)step), c2 = 1.0 - pow(beta2, (double)step);  // optim.py:73-74
+    const int64_t n4 = numel / 4;
+    k_adam<<<stream_grid(n4), kThreads, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<float4*>(w), reinterpret_cast<const float4*>(grad), reinterpret_cast<float4*>(m),
+        reinterpret_cast<float4*>(v), n4, (float)lr, (float)beta1, (float)beta2, (float)c1, (float)c2, (float)eps,
+        (float)weight_decay, guard_dev);
+    MBS_CK_LAUNCH("k_adam");
+    return MBS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,262 @@
+// K2: micro-batch staging — row gather + dtype cast + NCHW/NHWC layout, and a
+// byte-exact row gather for targets.
+//
+// Reference semantics: the epoch gather xb = x[order[start:start+M]]
+// (engine.py:310-312), the contiguous micro slice ascontiguousarray(x[lo:hi])
+// (engine.py:149-151) and the dtype coercion as_array (tensor.py:20-22). The
+// staged bytes are bit-identical to torch's x[rows].to(dtype[, channels_last]):
+// u8 -> f32/bf16/f16 is exact, f32 -> bf16 uses c10's round-to-nearest-even
+// (NaN -> 0x7FC0), f32 -> f16 uses cvt.rn.
+//
+// The source may be device memory or page-locked host memory (zero-copy over
+// PCIe); 128-bit loads and stores whenever the row base is 16-byte aligned.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mbs_common.h"
+
+namespace mbs {
+
+constexpr int kStageThreads = 256;
+constexpr int kPix = 16;  // pixels (NHWC) or elements (NCHW) per thread
+
+template <typename T> struct Elem;
+template <> struct Elem<uint8_t> { static __device__ __forceinline__ float f(uint8_t v) { return (float)v; } };
+template <> struct Elem<float> { static __device__ __forceinline__ float f(float v) { return v; } };
+template <> struct Elem<double> { static __device__ __forceinline__ float f(double v) { return __double2float_rn(v); } };
+
+__device__ __forceinline__ uint16_t f32_to_bf16_rne(float f) {
+    // identical to c10::BFloat16 round_to_nearest_even
+    if (f != f) return 0x7FC0u;
+    const uint32_t u = __float_as_uint(f);
+    const uint32_t bias = ((u >> 16) & 1u) + 0x7FFFu;
+    return (uint16_t)((u + bias) >> 16);
+}
+
+template <int OUT> struct Out;
+template <> struct Out<MBS_F32> {
+    using T = float;
+    static __device__ __forceinline__ T cvt(float v) { return v; }
+};
+template <> struct Out<MBS_BF16> {
+    using T = uint16_t;
+    static __device__ __forceinline__ T cvt(float v) { return f32_to_bf16_rne(v); }
+};
+template <> struct Out<MBS_F16> {
+    using T = uint16_t;
+    static __device__ __forceinline__ T cvt(float v) { return __half_as_ushort(__float2half_rn(v)); }
+};
+
+__device__ __forceinline__ int64_t src_row(const int64_t* rows, int64_t row0, int64_t r) {
+    return rows ? rows[r] : row0 + r;
+}
+
+// Load kPix consecutive source elements as floats (vector path when aligned).
+template <typename TI>
+__device__ __forceinline__ void load_pix(const TI* p, float* v, bool vec) {
+    if (vec) {
+        if constexpr (sizeof(TI) == 1) {
+            const uint4 q = *reinterpret_cast<const uint4*>(p);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = (float)((w[i >> 2] >> ((i & 3) * 8)) & 0xFFu);
+        } else if constexpr (sizeof(TI) == 8) {
+#pragma unroll
+            for (int j = 0; j < kPix / 2; ++j) {
+                const double2 q = reinterpret_cast<const double2*>(p)[j];
+                v[2 * j] = __double2float_rn(q.x); v[2 * j + 1] = __double2float_rn(q.y);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kPix / 4; ++j) {
+                const float4 q = reinterpret_cast<const float4*>(p)[j];
+                v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < kPix; ++i) v[i] = Elem<TI>::f(p[i]);
+    }
+}
+
+template <typename TO>
+__device__ __forceinline__ void store_vec(TO* dst, const TO* vals, int n, bool vec) {
+    // n elements, 16-byte chunks when aligned
+    if (vec) {
+        constexpr int per = 16 / sizeof(TO);
+        for (int j = 0; j < n / per; ++j) {
+            uint4 q;
+            memcpy(&q, vals + j * per, 16);
+            reinterpret_cast<uint4*>(dst)[j] = q;
+        }
+    } else {
+        for (int i = 0; i < n; ++i) dst[i] = vals[i];
+    }
+}
+
+// NCHW -> NCHW (cast only): thread handles kPix consecutive elements of one row.
+template <typename TI, int OUT>
+__global__ void __launch_bounds__(kStageThreads)
+k_stage_nchw(const TI* __restrict__ src, const int64_t* __restrict__ rows, int64_t row0, int64_t E,
+             typename Out<OUT>::T* __restrict__ dst, bool vec_ok) {
+    using TO = typename Out<OUT>::T;
+    const int64_t r = blockIdx.y;
+    const int64_t e0 = ((int64_t)blockIdx.x * kStageThreads + threadIdx.x) * kPix;
+    if (e0 >= E) return;
+    const TI* s = src + src_row(rows, row0, r) * E + e0;
+    TO* d = dst + r * E + e0;
+    if (vec_ok && e0 + kPix <= E) {
+        float v[kPix];
+        load_pix<TI>(s, v, true);
+        TO o[kPix];
+#pragma unroll
+        for (int i = 0; i < kPix; ++i) o[i] = Out<OUT>::cvt(v[i]);
+        store_vec<TO>(d, o, kPix, true);
+    } else {
+        const int64_t n = min((int64_t)kPix, E - e0);
+        for (int64_t i = 0; i < n; ++i) d[i] = Out<OUT>::cvt(Elem<TI>::f(s[i]));
+    }
+}
+
+// NCHW -> NHWC: thread handles kPix consecutive pixels x all C (C <= 4) channels.
+template <typename TI, int OUT, int C>
+__global__ void __launch_bounds__(kStageThreads)
+k_stage_nhwc(const TI* __restrict__ src, const int64_t* __restrict__ rows, int64_t row0, int64_t HW,
+             typename Out<OUT>::T* __restrict__ dst, bool vec_ok) {
+    using TO = typename Out<OUT>::T;
+    const int64_t r = blockIdx.y;
+    const int64_t p0 = ((int64_t)blockIdx.x * kStageThreads + threadIdx.x) * kPix;
+    if (p0 >= HW) return;
+    const TI* s = src + src_row(rows, row0, r) * (int64_t)C * HW;
+    TO* d = dst + (r * HW + p0) * C;
+    if (vec_ok && p0 + kPix <= HW) {
+        TO o[kPix * C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            float v[kPix];
+            load_pix<TI>(s + c * HW + p0, v, true);
+#pragma unroll
+            for (int i = 0; i < kPix; ++i) o[i * C + c] = Out<OUT>::cvt(v[i]);
+        }
+        store_vec<TO>(d, o, kPix * C, true);
+    } else {
+        const int64_t n = min((int64_t)kPix, HW - p0);
+        for (int64_t i = 0; i < n; ++i)
+            for (int c = 0; c < C; ++c) d[i * C + c] = Out<OUT>::cvt(Elem<TI>::f(s[c * HW + p0 + i]));
+    }
+}
+
+// Generic NHWC for any C (scalar; one thread per output element).
+template <typename TI, int OUT>
+__global__ void __launch_bounds__(kStageThreads)
+k_stage_nhwc_generic(const TI* __restrict__ src, const int64_t* __restrict__ rows, int64_t row0, int64_t C,
+                     int64_t HW, typename Out<OUT>::T* __restrict__ dst) {
+    const int64_t r = blockIdx.y;
+    const int64_t e = (int64_t)blockIdx.x * kStageThreads + threadIdx.x;
+    if (e >= C * HW) return;
+    const int64_t p = e / C, c = e % C;
+    dst[r * C * HW + e] = Out<OUT>::cvt(Elem<TI>::f(src[src_row(rows, row0, r) * C * HW + c * HW + p]));
+}
+
+template <typename V>
+__global__ void __launch_bounds__(kStageThreads)
+k_gather_rows(const V* __restrict__ src, const int64_t* __restrict__ rows, int64_t row0, int64_t nv,
+              V* __restrict__ dst) {
+    const int64_t r = blockIdx.y;
+    const V* s = src + src_row(rows, row0, r) * nv;
+    V* d = dst + r * nv;
+    for (int64_t i = (int64_t)blockIdx.x * kStageThreads + threadIdx.x; i < nv; i += (int64_t)gridDim.x * kStageThreads)
+        d[i] = s[i];
+}
+
+template <typename TI, int OUT>
+static int stage_typed(const void* src, const int64_t* rows, int64_t row0, int64_t n_rows, int64_t C, int64_t H,
+                       int64_t W, void* dst, int layout, cudaStream_t st) {
+    using TO = typename Out<OUT>::T;
+    const int64_t HW = H * W, E = C * HW;
+    const auto* s = static_cast<const TI*>(src);
+    auto* d = static_cast<TO*>(dst);
+    const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
+    if (n_rows > 65535) return invalid("mbs_stage: at most 65535 rows per call");
+    if (layout == MBS_NCHW || C == 1) {
+        // vector path needs 16-byte aligned rows in both src and dst
+        const bool vec = (sa % 16 == 0) && (da % 16 == 0) && ((E * (int64_t)sizeof(TI)) % 16 == 0) &&
+                         ((E * (int64_t)sizeof(TO)) % 16 == 0) && ((kPix * sizeof(TO)) % 16 == 0);
+        dim3 grid((unsigned)((E + (int64_t)kStageThreads * kPix - 1) / ((int64_t)kStageThreads * kPix)), (unsigned)n_rows);
+        k_stage_nchw<TI, OUT><<<grid, kStageThreads, 0, st>>>(s, rows, row0, E, d, vec);
+    } else if (layout == MBS_NHWC && C <= 4) {
+        const bool vec = (sa % 16 == 0) && (da % 16 == 0) && ((HW * (int64_t)sizeof(TI)) % 16 == 0) &&
+                         ((kPix * C * sizeof(TO)) % 16 == 0) && ((E * (int64_t)sizeof(TO)) % 16 == 0);
+        dim3 grid((unsigned)((HW + (int64_t)kStageThreads * kPix - 1) / ((int64_t)kStageThreads * kPix)), (unsigned)n_rows);
+        switch (C) {
+            case 2: k_stage_nhwc<TI, OUT, 2><<<grid, kStageThreads, 0, st>>>(s, rows, row0, HW, d, vec); break;
+            case 3: k_stage_nhwc<TI, OUT, 3><<<grid, kStageThreads, 0, st>>>(s, rows, row0, HW, d, vec); break;
+            default: k_stage_nhwc<TI, OUT, 4><<<grid, kStageThreads, 0, st>>>(s, rows, row0, HW, d, vec); break;
+        }
+    } else if (layout == MBS_NHWC) {
+        dim3 grid((unsigned)((E + kStageThreads - 1) / kStageThreads), (unsigned)n_rows);
+        k_stage_nhwc_generic<TI, OUT><<<grid, kStageThreads, 0, st>>>(s, rows, row0, C, HW, d);
+    } else {
+        return invalid("mbs_stage: unknown layout");
+    }
+    MBS_CK_LAUNCH("k_stage");
+    return MBS_OK;
+}
+
+}  // namespace mbs
+
+using namespace mbs;
+
+extern "C" {
+
+int mbs_stage(const void* src, int src_dtype, const int64_t* rows, int64_t row0, int64_t n_rows, int64_t C,
+              int64_t H, int64_t W, void* dst, int dst_dtype, int dst_layout, void* stream) {
+    if (!src || !dst || n_rows < 0 || C < 1 || H < 1 || W < 1 || (!rows && row0 < 0))
+        return invalid("mbs_stage: bad arguments");
+    if (n_rows == 0) return MBS_OK;
+    auto st = (cudaStream_t)stream;
+    if (src_dtype == MBS_U8) {
+        if (dst_dtype == MBS_F32) return stage_typed<uint8_t, MBS_F32>(src, rows, row0, n_rows, C, H, W, dst, dst_layout, st);
+        if (dst_dtype == MBS_BF16) return stage_typed<uint8_t, MBS_BF16>(src, rows, row0, n_rows, C, H, W, dst, dst_layout, st);
+        if (dst_dtype == MBS_F16) return stage_typed<uint8_t, MBS_F16>(src, rows, row0, n_rows, C, H, W, dst, dst_layout, st);
+    } else if (src_dtype == MBS_F32) {
+        if (dst_dtype == MBS_F32) return stage_typed<float, MBS_F32>(src, rows, row0, n_rows, C, H, W, dst, dst_layout, st);
+        if (dst_dtype == MBS_BF16) return stage_typed<float, MBS_BF16>(src, rows, row0, n_rows, C, H, W, dst, dst_layout, st);
+        if (dst_dtype == MBS_F16) return stage_typed<float, MBS_F16>(src, rows, row0, n_rows, C, H, W, dst, dst_layout, st);
+    } else if (src_dtype == MBS_F64) {
+        if (dst_dtype == MBS_F32) return stage_typed<double, MBS_F32>(src, rows, row0, n_rows, C, H, W, dst, dst_layout, st);
+        if (dst_dtype == MBS_BF16) return stage_typed<double, MBS_BF16>(src, rows, row0, n_rows, C, H, W, dst, dst_layout, st);
+        if (dst_dtype == MBS_F16) return stage_typed<double, MBS_F16>(src, rows, row0, n_rows, C, H, W, dst, dst_layout, st);
+    }
+    return invalid("mbs_stage: unsupported dtype pair");
+}
+
+int mbs_gather_rows(const void* src, const int64_t* rows, int64_t row0, int64_t n_rows, int64_t row_bytes, void* dst,
+                    void* stream) {
+    if (!src || !dst || n_rows < 0 || row_bytes < 1 || (!rows && row0 < 0)) return invalid("mbs_gather_rows: bad arguments");
+    if (n_rows == 0) return MBS_OK;
+    if (n_rows > 65535) return invalid("mbs_gather_rows: at most 65535 rows per call");
+    auto st = (cudaStream_t)stream;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst);
+    auto grid_for = [&](int64_t nv) {
+        return dim3((unsigned)std::min<int64_t>((nv + kStageThreads - 1) / kStageThreads, 1024), (unsigned)n_rows);
+    };
+    if (a % 16 == 0 && row_bytes % 16 == 0) {
+        const int64_t nv = row_bytes / 16;
+        k_gather_rows<uint4><<<grid_for(nv), kStageThreads, 0, st>>>((const uint4*)src, rows, row0, nv, (uint4*)dst);
+    } else if (a % 8 == 0 && row_bytes % 8 == 0) {
+        const int64_t nv = row_bytes / 8;
+        k_gather_rows<uint2><<<grid_for(nv), kStageThreads, 0, st>>>((const uint2*)src, rows, row0, nv, (uint2*)dst);
+    } else if (a % 4 == 0 && row_bytes % 4 == 0) {
+        const int64_t nv = row_bytes / 4;
+        k_gather_rows<uint32_t><<<grid_for(nv), kStageThreads, 0, st>>>((const uint32_t*)src, rows, row0, nv, (uint32_t*)dst);
+    } else {
+        k_gather_rows<uint8_t><<<grid_for(row_bytes), kStageThreads, 0, st>>>((const uint8_t*)src, rows, row0, row_bytes, (uint8_t*)dst);
+    }
+    MBS_CK_LAUNCH("k_gather_rows");
+    return MBS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,239 @@
+"""Data-parallel MBS across the GPUs of one node: one all-reduce per mini-batch.
+
+The reference is single-device; this layer is new. The
+micro-batches of one mini-batch are independent until the sum
+(``engine.py:206-216``, Eq. 13), so the GLOBAL plan ``plan_split(N_B, N_mu)``
+is partitioned into contiguous blocks of whole micro-batches, one block per
+rank (at most one micro-batch of imbalance). Each rank:
+
+1. streams its own micro-batches and accumulates them with K1 using the
+   GLOBAL normalisation factors (``size_k / N_B`` or ``1 / N_Smu``) — so BN
+   micro-batch membership, and therefore every per-micro gradient, is exactly
+   the single-device one;
+2. on its LAST micro-batch, accumulates gradient BUCKETS as autograd produces
+   them (post-accumulate-grad hooks) and immediately launches an async NCCL
+   SUM all-reduce of that bucket's slice of the flat accumulator, so the
+   all-reduce overlaps the rest of the backward;
+3. after the last bucket, recomputes the grad norm of the reduced sum (the
+   optimizer's non-finite guard), all-reduces the tiny loss record, and runs
+   the identical K3 step on every rank.
+
+The pure functions (partition, factors, buckets, stats combination) carry the
+logic and are exercised on CPU with the gloo backend (tests/test_dp_gloo.py).
+"""
+
+from __future__ import annotations
+
+import math
+from contextlib import nullcontext
+
+import numpy as np
+import torch
+
+from .engine import (GradientAccumulator, MicroBatchPlan, MiniBatchStats, normalization_factor, plan_split,
+                     _as_tensor, _micro_source, make_streamer)
+from .losses import compute_loss
+from .optim import apply_update
+from .tensor import ParameterSet
+
+
+def partition_micro_batches(plan: MicroBatchPlan, world: int) -> list:
+    """Contiguous blocks of whole micro-batch indices per rank: [(k0, k1), ...] (at most 1 of imbalance)."""
+    if world < 1:
+        raise ValueError("world size must be positive")
+    q, r = divmod(plan.n_s_mu, world)
+    out, k = [], 0
+    for i in range(world):
+        n = q + (1 if i < r else 0)
+        out.append((k, k + n))
+        k += n
+    return out
+
+
+def rank_samples(plan: MicroBatchPlan, block: tuple) -> tuple:
+    """Global sample range [lo, hi) covered by a block of micro-batches."""
+    k0, k1 = block
+    if k1 <= k0:
+        return (0, 0)
+    return (plan.index_ranges[k0][0], plan.index_ranges[k1 - 1][1])
+
+
+def local_factors(plan: MicroBatchPlan, block: tuple, mode: str) -> list:
+    """GLOBAL normalisation factors of this rank's micro-batches (engine.py:81-91 on the global plan)."""
+    return [normalization_factor(plan, k, mode) for k in range(*block)]
+
+
+def weak_scaling_plan(n_b_per_rank: int, n_mu: int, world: int) -> MicroBatchPlan:
+    """Global plan when every rank holds its own n_b_per_rank samples (must split on micro boundaries)."""
+    if world > 1 and n_b_per_rank % n_mu:
+        raise ValueError("weak scaling needs the per-rank mini-batch to be a multiple of the micro-batch")
+    return plan_split(n_b_per_rank * world, n_mu)
+
+
+def bucket_ranges(numels: tuple, bucket_elems: int) -> list:
+    """Contiguous segment ranges [(s0, s1), ...] of ~bucket_elems, listed from the LAST segment backwards
+    (the order autograd produces gradients in)."""
+    out, hi, acc = [], len(numels), 0
+    for i in range(len(numels) - 1, -1, -1):
+        acc += numels[i]
+        if acc >= bucket_elems:
+            out.append((i, hi))
+            hi, acc = i, 0
+    if hi > 0:
+        out.append((0, hi))
+    return out
+
+
+def combine_loss_record(losses_local: list, factors_local: list, weights_local: list, block: tuple, n_s_mu: int,
+                        n_b: int) -> np.ndarray:
+    """Per-rank vector [lsum/N_B, raw losses (global slots), normalised losses] to be SUM-all-reduced."""
+    v = np.zeros(1 + 2 * n_s_mu)
+    k0, _ = block
+    for j, (l, f, wgt) in enumerate(zip(losses_local, factors_local, weights_local)):
+        v[0] += wgt * l
+        v[1 + k0 + j] = l
+        v[1 + n_s_mu + k0 + j] = l * f
+    v[0] /= n_b
+    return v
+
+
+class _Result:
+    """MiniBatchStats-compatible view of the combined global statistics."""
+
+    def __init__(self, vec_dev: torch.Tensor, norm2_dev: torch.Tensor, n_s_mu: int):
+        self._n = n_s_mu
+        self._host = torch.empty(vec_dev.numel() + 1, dtype=torch.float64, pin_memory=True)
+        self._host[:-1].copy_(vec_dev, non_blocking=True)
+        self._host[-1:].copy_(norm2_dev.reshape(1), non_blocking=True)
+        self._ev = torch.cuda.Event()
+        self._ev.record()
+        self.step_count = 0
+        self._r = None
+
+    def resolve(self):
+        if self._r is None:
+            self._ev.synchronize()
+            h = self._host.tolist()
+            n = self._n
+            self._r = dict(loss=h[0], losses_raw=h[1:1 + n], losses_normalized=h[1 + n:1 + 2 * n], norm2=h[-1])
+            if not math.isfinite(h[-1]):
+                from .errors import NonFiniteError
+                raise NonFiniteError(-1, "non-finite accumulated gradient; the optimizer step was skipped")
+        return self._r
+
+    loss = property(lambda s: s.resolve()["loss"])
+    losses_raw = property(lambda s: s.resolve()["losses_raw"])
+    losses_normalized = property(lambda s: s.resolve()["losses_normalized"])
+    grad_norm = property(lambda s: math.sqrt(s.resolve()["norm2"]))
+    n_micro = property(lambda s: s._n)
+    outputs = None
+
+
+class DataParallelMBS:
+    """Per-rank driver of data-parallel micro-batch streaming (torch.distributed, NCCL)."""
+
+    def __init__(self, params: ParameterSet, process_group=None, bucket_mb: float = 32.0):
+        import torch.distributed as dist
+        self.dist = dist
+        self.params = params
+        self.group = process_group
+        self.world = dist.get_world_size(process_group)
+        self.rank = dist.get_rank(process_group)
+        self.buckets = bucket_ranges(params.layout.numels, max(1, int(bucket_mb * 2 ** 20 / 4)))
+        self._seg_bucket = {}
+        for b, (s0, s1) in enumerate(self.buckets):
+            for s in range(s0, s1):
+                self._seg_bucket[s] = b
+
+    def _slice(self, acc: GradientAccumulator, s0: int, s1: int) -> torch.Tensor:
+        lay = acc.layout
+        lo = lay.offsets[s0]
+        hi = lay.offsets[s1 - 1] + lay.numels[s1 - 1]
+        return acc.flat[lo:hi]
+
+    def train_mini_batch(self, model, batch, n_b_per_rank: int, n_mu: int, normalization: str, loss_kind: str,
+                         optimizer_state, *, accumulator: GradientAccumulator, staging=None, autocast_dtype=None,
+                         streamer=None, prefetch=True, loss_from_logits=True, dice_smoothing=1.0):
+        """Weak-scaling step: this rank's batch holds its own n_b_per_rank samples (= its block of the global plan)."""
+        plan = weak_scaling_plan(n_b_per_rank, n_mu, self.world)
+        block = partition_micro_batches(plan, self.world)[self.rank]
+        lo, hi = rank_samples(plan, block)
+        x, y = (_as_tensor(t) for t in batch)
+        if x.shape[0] != hi - lo:
+            raise ValueError(f"rank {self.rank} holds {x.shape[0]} samples, its block of the plan needs {hi - lo}")
+        acc = accumulator
+        n_local = block[1] - block[0]
+        acc.begin(n_local)
+        jobs = [(None, plan.index_ranges[k][0] - lo, plan.sizes[k]) for k in range(*block)]
+        own = None
+        if x.device.type == "cpu" and streamer is None:
+            streamer = own = make_streamer(x, y, n_mu)
+        source = _micro_source(x, y, jobs, staging, prefetch, streamer)
+        ctx = torch.autocast("cuda", dtype=autocast_dtype) if autocast_dtype is not None else nullcontext()
+        model.train()
+        losses, factors, weights = [], [], []
+        works = []
+        plist = acc._plist
+        for j, (xk, yk) in enumerate(source):
+            k = block[0] + j
+            f = normalization_factor(plan, k, normalization)
+            last = j == n_local - 1
+            with ctx:
+                out = model(xk)
+                loss = compute_loss(loss_kind, out, yk, from_logits=loss_from_logits, dice_smoothing=dice_smoothing)
+            losses.append(loss.detach().float())
+            factors.append(f)
+            weights.append(float(plan.sizes[k]))
+            if not last:
+                loss.backward()
+                acc.add_module_grads(f, loss=loss, loss_factor=f, loss_weight=plan.sizes[k])
+                continue
+            # last micro-batch: bucket-wise K1 + async all-reduce, overlapped with the rest of backward
+            pending = {b: s1 - s0 for b, (s0, s1) in enumerate(self.buckets)}
+            handles = []
+
+            def hook(p, _idx={id(q): i for i, q in enumerate(plist)}):
+                s = _idx[id(p)]
+                b = self._seg_bucket[s]
+                pending[b] -= 1
+                if pending[b] == 0:
+                    s0, s1 = self.buckets[b]
+                    acc.add_tensors([plist[i].grad for i in range(s0, s1)], f, seg_begin=s0, last=False,
+                                    loss=loss if s0 == 0 else None, loss_factor=f, loss_weight=plan.sizes[k])
+                    for i in range(s0, s1):
+                        plist[i].grad = None
+                    works.append(self.dist.all_reduce(self._slice(acc, s0, s1), group=self.group, async_op=True))
+
+            for p in plist:
+                handles.append(p.register_post_accumulate_grad_hook(hook))
+            try:
+                loss.backward()
+            finally:
+                for h in handles:
+                    h.remove()
+            if any(v != 0 for v in pending.values()):
+                from .errors import AccumulatorOverflowError
+                raise AccumulatorOverflowError("a parameter received no gradient on the last micro-batch")
+        if own is not None:
+            own.close()
+        for wk in works:
+            wk.wait()
+        if n_local == 0:
+            acc.begin(0)
+        # grad norm of the REDUCED sum (the optimizer's guard) + the global loss record
+        stats_dev = acc.finalize(plan.n_b, recompute_norm=True)
+        rec = torch.zeros(1 + 2 * plan.n_s_mu, dtype=torch.float64, device=acc.flat.device)
+        if losses:
+            lv = torch.stack(losses).double()
+            k0 = block[0]
+            wv = torch.tensor(weights, dtype=torch.float64, device=lv.device)
+            fv = torch.tensor(factors, dtype=torch.float64, device=lv.device)
+            rec[0] = (wv * lv).sum() / plan.n_b
+            rec[1 + k0:1 + k0 + n_local] = lv
+            rec[1 + plan.n_s_mu + k0:1 + plan.n_s_mu + k0 + n_local] = lv * fv
+        self.dist.all_reduce(rec, group=self.group)
+        total = acc.as_gradient_set()
+        apply_update(self.params, total, optimizer_state)
+        res = _Result(rec, stats_dev[0], plan.n_s_mu)
+        res.step_count = optimizer_state.step_count
+        return res

@@ -1,0 +1,557 @@
+"""Micro-batch streaming training loop on the B200 — the reference's ``engine.py`` API.
+
+Same functions, argument meaning and exceptions as the reference
+(``engine.py:37-335``): ``plan_split``, ``normalization_factor``,
+``normalize_loss``, ``GradientAccumulator``, ``accumulate``,
+``mini_batch_gradient``, ``train_mini_batch``, ``train_epoch``. What changes
+is where the work runs:
+
+* the model is a torch ``nn.Module`` whose forward/backward stay on
+  cuDNN/cuBLAS (optionally under autocast);
+* micro-batches come from HBM (K2 staging) or from host memory through the
+  pinned H2D streamer (``streamer.py``);
+* the per-micro normalise-and-accumulate is ONE fused sm_100a kernel over the
+  flat gradient (K1, ``mbs_accum_add``): ``acc = s*g`` on the first
+  micro-batch of a mini-batch (the zero of ``begin`` folded in),
+  ``acc += s*g`` afterwards, with the grad-norm partials and the loss record
+  fused into the last pass; the optimizer is one fused flat pass (K3);
+* the loss / grad-norm statistics stay on device until read: there is no
+  host synchronisation inside the micro loop.
+
+``normalize_via``: the reference folds the factor into the backward seed
+(``"seed"``, ``engine.py:214-215``) or scales the recorded loss
+(``"loss_scale"``, ``engine.py:211-213``). Both remain available; the default
+``"fused"`` runs backward with seed 1 and applies the factor inside K1. All
+three are the same linear map (``backward`` is linear in the seed), so the
+accumulated gradients agree to fp32 rounding (tests/test_engine_gpu.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from contextlib import nullcontext
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import AccumulatorOverflowError, GradientKeyMismatchError, NonFiniteError
+from .losses import LossValue, compute_loss
+from .optim import OptimizerState, apply_update
+from .prof import TIMER
+from .rng import epoch_order
+from .streamer import MicroBatchStreamer, Staging, device_micro_batches
+from .tensor import GradientSet, ParameterSet
+
+NORMALIZATION_MODES = ("paper_faithful", "exact_weighted", "off")  # engine.py:34
+NORMALIZE_VIA = ("fused", "seed", "loss_scale")
+
+
+# ---------------------------------------------------------------------------
+# Plan (engine.py:37-97)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class MicroBatchPlan:
+    """Ordered split of one mini-batch into contiguous micro-batches (engine.py:37-53)."""
+
+    n_b: int
+    n_mu: int
+    n_s_mu: int
+    sizes: tuple
+    index_ranges: tuple
+
+    def __post_init__(self):
+        if sum(self.sizes) != self.n_b:
+            raise ValueError("micro-batch sizes must cover the mini-batch exactly")
+        if any(s < 1 or s > self.n_mu for s in self.sizes):
+            raise ValueError("every micro-batch size must lie in [1, n_mu]")
+        if len(self.sizes) != self.n_s_mu or len(self.index_ranges) != self.n_s_mu:
+            raise ValueError("plan length disagrees with n_s_mu")
+
+
+def plan_split(n_b: int, n_mu: int) -> MicroBatchPlan:
+    """Split n_b samples into micro-batches of at most n_mu (engine.py:56-78), via ``mbs_plan_split``."""
+    L = N.lib()
+    nm, ns = ctypes.c_int64(), ctypes.c_int64()
+    N.check(L.mbs_plan_split(int(n_b), int(n_mu), ctypes.byref(nm), ctypes.byref(ns), None, 0), "plan_split")
+    sizes = (ctypes.c_int64 * ns.value)()
+    N.check(L.mbs_plan_split(int(n_b), int(n_mu), None, None, sizes, ns.value), "plan_split")
+    sizes = tuple(int(s) for s in sizes)
+    ranges, start = [], 0
+    for s in sizes:
+        ranges.append((start, start + s))
+        start += s
+    return MicroBatchPlan(n_b=int(n_b), n_mu=nm.value, n_s_mu=ns.value, sizes=sizes, index_ranges=tuple(ranges))
+
+
+def normalization_factor(plan: MicroBatchPlan, k: int, mode: str) -> float:
+    """Scale applied to micro-batch k's loss before backward (engine.py:81-91)."""
+    if not 0 <= k < plan.n_s_mu:
+        raise ValueError(f"micro-batch index {k} outside plan of {plan.n_s_mu}")
+    if mode == "paper_faithful":
+        return 1.0 / plan.n_s_mu
+    if mode == "exact_weighted":
+        return plan.sizes[k] / plan.n_b
+    if mode == "off":
+        return 1.0
+    raise ValueError(f"unknown normalization mode {mode!r}")
+
+
+def normalize_loss(loss: LossValue, plan: MicroBatchPlan, k: int, mode: str) -> LossValue:
+    """engine.py:94-97."""
+    factor = normalization_factor(plan, k, mode)
+    return LossValue(value=loss.value * factor, n_samples=loss.n_samples)
+
+
+# ---------------------------------------------------------------------------
+# Gradient accumulator (engine.py:100-137) — K1
+# ---------------------------------------------------------------------------
+
+def _stream_ptr(stream=None) -> int:
+    return (stream or torch.cuda.current_stream()).cuda_stream
+
+
+class GradientAccumulator:
+    """Running fp32 sum of micro-batch gradients in one flat HBM buffer (engine.py:100-131).
+
+    ``sums`` / ``as_gradient_set()`` alias the live buffer (as the reference's
+    do). ``begin`` is lazy: the next ``add`` assigns instead of
+    accumulating, so no zero pass is ever paid on the hot path.
+    """
+
+    DEFAULT_MAX_MICRO = 1 << 16
+
+    def __init__(self, params: ParameterSet, expected: int | None = None, *, max_micro: int | None = None):
+        if not isinstance(params, ParameterSet):
+            raise TypeError("GradientAccumulator needs a paper_2110_12484_b200.ParameterSet")
+        self.params = params
+        self.layout = params.layout
+        self.max_micro = int(max_micro or self.DEFAULT_MAX_MICRO)
+        self.flat = torch.zeros(self.layout.total, dtype=torch.float32, device=params.device)
+        self.stats_dev = torch.zeros(4 + 2 * self.max_micro, dtype=torch.float64, device=params.device)
+        offs = N.i64_array(self.layout.offsets)
+        nums = N.i64_array(self.layout.numels)
+        h = ctypes.c_void_p()
+        N.check(N.lib().mbs_accum_create(self.flat.data_ptr(), self.layout.total, len(self.layout.names), offs, nums,
+                                         self.max_micro, ctypes.byref(h)), "mbs_accum_create")
+        self._h = h
+        self._views = self.layout.views(self.flat)
+        self._plist = [params[n] for n in self.layout.names]
+        self._pending_zero = False
+        self._fresh = True
+        self._covered = 0
+        self.expected = expected
+        if expected is not None:
+            self.begin(expected)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                torch.cuda.synchronize(self.flat.device)
+                N.lib().mbs_accum_destroy(h)
+            except Exception:
+                pass
+
+    # -- reference surface --
+    @property
+    def micro_batches_seen(self) -> int:
+        seen = ctypes.c_int64()
+        N.check(N.lib().mbs_accum_seen(self._h, ctypes.byref(seen), None), "mbs_accum_seen")
+        return seen.value
+
+    @property
+    def sums(self) -> dict:
+        self._materialize()
+        return dict(self._views)
+
+    def begin(self, expected: int) -> None:
+        """Reset for the next mini-batch (engine.py:110-115); the zero is folded into the next add."""
+        if expected is not None and expected > self.max_micro:
+            raise ValueError(f"{expected} micro-batches exceed max_micro={self.max_micro}")
+        N.check(N.lib().mbs_accum_begin(self._h, -1 if expected is None else int(expected)), "mbs_accum_begin")
+        self.expected = expected
+        self._pending_zero = True
+        self._fresh = True
+        self._covered = 0
+
+    def add(self, grads: GradientSet | dict) -> None:
+        """sums += grads in parameter order (engine.py:117-128)."""
+        arrays = grads.arrays if isinstance(grads, GradientSet) else dict(grads)
+        if set(arrays) != set(self.layout.names):
+            raise AccumulatorOverflowError("gradient keys do not match accumulator parameters")
+        tensors = []
+        for i, n in enumerate(self.layout.names):
+            g = arrays[n]
+            if tuple(g.shape) != self.layout.shapes[i]:
+                raise GradientKeyMismatchError(f"gradient shape {tuple(g.shape)} != parameter shape "
+                                               f"{self.layout.shapes[i]} for {n!r}")
+            tensors.append(g)
+        self.add_tensors(tensors, 1.0)
+
+    def as_gradient_set(self) -> GradientSet:
+        """engine.py:130-131 — a GradientSet ALIASING the live sums."""
+        self._materialize()
+        return GradientSet(dict(self._views), flat=self.flat, layout=self.layout, norm2=self.stats_dev[0])
+
+    # -- B200 surface --
+    def _materialize(self):
+        if self._pending_zero and self.micro_batches_seen == 0:
+            N.check(N.lib().mbs_accum_zero(self._h, _stream_ptr()), "mbs_accum_zero")
+        self._pending_zero = False
+
+    def _conform(self, g: torch.Tensor, i: int) -> torch.Tensor:
+        shape, stride = self.layout.shapes[i], self.layout.strides[i]
+        if g.dtype == torch.float32 and g.device == self.flat.device and tuple(g.stride()) == stride:
+            return g
+        out = torch.empty_strided(shape, stride, dtype=torch.float32, device=self.flat.device)
+        out.copy_(g)
+        return out
+
+    def add_tensors(self, tensors: list, factor: float, *, loss: torch.Tensor | None = None,
+                    loss_factor: float | None = None, loss_weight: float = 0.0, last: bool = False,
+                    seg_begin: int = 0, stream=None) -> None:
+        """K1 over segments [seg_begin, seg_begin+len(tensors)): acc (+)= factor * g."""
+        n = len(tensors)
+        ptrs = (ctypes.c_void_p * n)()
+        keep = []
+        for j, g in enumerate(tensors):
+            g = self._conform(g, seg_begin + j)
+            keep.append(g)
+            ptrs[j] = g.data_ptr()
+        lp = None
+        if loss is not None:
+            loss = loss.detach()
+            if loss.dtype != torch.float32:
+                loss = loss.float()
+            keep.append(loss)
+            lp = loss.data_ptr()
+        lf = float(factor if loss_factor is None else loss_factor)
+        t0 = TIMER.start(stream)
+        N.check(N.lib().mbs_accum_add(self._h, ptrs, int(seg_begin), n, float(factor), lp, lf, float(loss_weight),
+                                      int(bool(last)), _stream_ptr(stream)), "mbs_accum_add")
+        if t0 is not None:
+            elems = sum(self.layout.numels[seg_begin:seg_begin + n])
+            TIMER.stop("k1_accumulate", t0, (8 if self._fresh else 12) * elems, stream)
+        self._covered += n
+        if self._covered >= len(self.layout.names):
+            self._covered = 0
+            self._fresh = False
+        self._pending_zero = False
+
+    def add_module_grads(self, factor: float, *, loss: torch.Tensor | None = None,
+                         loss_factor: float | None = None, loss_weight: float = 0.0, last: bool = False,
+                         stream=None) -> None:
+        """K1 straight from the module's ``.grad`` tensors, which are then released."""
+        grads = []
+        for p in self._plist:
+            if p.grad is None:
+                raise AccumulatorOverflowError("gradient keys do not match accumulator parameters "
+                                               "(a parameter received no gradient)")
+            grads.append(p.grad)
+        self.add_tensors(grads, factor, loss=loss, loss_factor=loss_factor, loss_weight=loss_weight, last=last,
+                         stream=stream)
+        for p in self._plist:
+            p.grad = None
+
+    def finalize(self, n_b: int, *, recompute_norm: bool = False, stream=None) -> torch.Tensor:
+        """Reduce the grad-norm partials and the loss record into ``stats_dev`` (device)."""
+        if recompute_norm:
+            t0 = TIMER.start(stream)
+            N.check(N.lib().mbs_accum_norm(self._h, _stream_ptr(stream)), "mbs_accum_norm")
+            TIMER.stop("k1_norm", t0, 4 * self.layout.n_params, stream)
+        t0 = TIMER.start(stream)
+        N.check(N.lib().mbs_accum_finalize(self._h, int(n_b), self.stats_dev.data_ptr(), _stream_ptr(stream)),
+                "mbs_accum_finalize")
+        TIMER.stop("k4_finalize", t0, 0, stream)
+        return self.stats_dev
+
+
+def accumulate(acc: GradientAccumulator, grads: GradientSet) -> GradientAccumulator:
+    """engine.py:134-137."""
+    acc.add(grads)
+    return acc
+
+
+# ---------------------------------------------------------------------------
+# Statistics (engine.py:166-176, 264-273) — resolved lazily, one D2H per mini-batch
+# ---------------------------------------------------------------------------
+
+class MiniBatchStats:
+    """Per-mini-batch observables (engine.py:166-176), copied off the device asynchronously.
+
+    Reading any field synchronises on that copy; a non-finite accumulated
+    gradient raises ``NonFiniteError`` there (the optimizer step was already
+    suppressed on device, so the parameters are intact).
+    """
+
+    def __init__(self, stats_dev: torch.Tensor, n_micro: int, max_micro: int, outputs: list, stream=None):
+        self._n = int(n_micro)
+        self._max = int(max_micro)
+        head = torch.cat([stats_dev[:4 + self._n], stats_dev[4 + self._max:4 + self._max + self._n]])
+        self._host = torch.empty(head.shape, dtype=torch.float64, pin_memory=True)
+        self._host.copy_(head, non_blocking=True)
+        self._event = torch.cuda.Event()
+        self._event.record(stream or torch.cuda.current_stream())
+        self._outputs = outputs
+        self._resolved = None
+        self.step_count = 0
+
+    def resolve(self) -> dict:
+        if self._resolved is None:
+            self._event.synchronize()
+            h = self._host.tolist()
+            n = self._n
+            self._resolved = dict(norm2=h[0], loss=h[1], nonfinite=h[2] != 0.0, losses_raw=h[4:4 + n],
+                                  losses_normalized=h[4 + n:4 + 2 * n])
+            if self._resolved["nonfinite"] or not all(math.isfinite(v) for v in self._resolved["losses_raw"]):
+                raise NonFiniteError(-1, "non-finite accumulated gradient or micro-batch loss; "
+                                         "the optimizer step was skipped")
+        return self._resolved
+
+    @property
+    def losses_raw(self) -> list:
+        return self.resolve()["losses_raw"]
+
+    @property
+    def losses_normalized(self) -> list:
+        return self.resolve()["losses_normalized"]
+
+    @property
+    def loss(self) -> float:
+        return self.resolve()["loss"]
+
+    @property
+    def grad_norm(self) -> float:
+        return math.sqrt(self.resolve()["norm2"])
+
+    @property
+    def n_micro(self) -> int:
+        return self._n
+
+    @property
+    def outputs(self) -> torch.Tensor | None:
+        if not self._outputs:
+            return None
+        if len(self._outputs) > 1:
+            self._outputs = [torch.cat(self._outputs, dim=0)]
+        return self._outputs[0]
+
+
+@dataclass
+class EpochStats:
+    """engine.py:264-273."""
+
+    mini_losses: list
+    mean_loss: float
+    mini_metrics: list
+    mini_sizes: list
+    step_count: int
+    mini_stats: list = field(default_factory=list)
+
+
+# ---------------------------------------------------------------------------
+# The micro loop (engine.py:179-230)
+# ---------------------------------------------------------------------------
+
+def _as_tensor(a):
+    if isinstance(a, torch.Tensor):
+        return a
+    return torch.from_numpy(np.ascontiguousarray(a))
+
+
+def _micro_source(x, y, jobs, staging, prefetch, streamer):
+    if x.device.type == "cuda":
+        return device_micro_batches(x, y.to(x.device) if y.device != x.device else y, jobs, staging)
+    if streamer is None:
+        raise ValueError("host-resident inputs need a MicroBatchStreamer (pass streamer=...)")
+    return streamer.stream(x, y, jobs, staging, prefetch=prefetch)
+
+
+def make_streamer(x: torch.Tensor, y: torch.Tensor, max_rows: int, *, n_slots: int = 3, n_threads=None):
+    """A streamer sized for micro-batches of up to ``max_rows`` rows of x / y."""
+    xr = x.element_size() * int(np.prod(x.shape[1:]))
+    yr = y.element_size() * int(np.prod(y.shape[1:])) if y.dim() > 1 else y.element_size()
+    return MicroBatchStreamer(xr, yr, max_rows, n_slots=n_slots, n_threads=n_threads)
+
+
+def mini_batch_gradient(model: torch.nn.Module, params: ParameterSet, x, y, plan: MicroBatchPlan,
+                        normalization: str = "paper_faithful", loss_kind: str = "mse", *,
+                        loss_from_logits: bool = True, dice_smoothing: float = 1.0, prefetch: bool = False,
+                        accumulator: GradientAccumulator | None = None, normalize_via: str = "fused",
+                        forward_mode: str = "train", staging: Staging | None = None,
+                        autocast_dtype: torch.dtype | None = None, streamer: MicroBatchStreamer | None = None,
+                        keep_outputs: bool = True) -> tuple:
+    """Accumulated gradient of one mini-batch, micro-batch by micro-batch (engine.py:179-230).
+
+    ``x``/``y`` are device tensors (sliced / staged in HBM) or host tensors
+    (streamed through ``streamer``; one is created when omitted). Returns
+    (GradientSet aliasing the accumulator, MiniBatchStats).
+    """
+    x, y = _as_tensor(x), _as_tensor(y)
+    if x.shape[0] != plan.n_b:
+        raise ValueError(f"batch has {x.shape[0]} samples but plan expects {plan.n_b}")
+    if normalize_via not in NORMALIZE_VIA:
+        raise ValueError(f"unknown normalize_via {normalize_via!r}")
+    if normalization not in NORMALIZATION_MODES:
+        raise ValueError(f"unknown normalization mode {normalization!r}")
+    if forward_mode not in ("train", "eval"):
+        raise ValueError(f"mode must be 'train' or 'eval', got {forward_mode!r}")
+    acc = accumulator if accumulator is not None else GradientAccumulator(params)
+    acc.begin(plan.n_s_mu)
+    model.train(forward_mode == "train")
+    own_streamer = None
+    if x.device.type == "cpu" and streamer is None:
+        streamer = own_streamer = make_streamer(x, y, plan.n_mu)
+    jobs = [(None, lo, hi - lo) for lo, hi in plan.index_ranges]
+    try:
+        source = _micro_source(x, y, jobs, staging, prefetch, streamer)
+        outputs = _run_micro_loop(model, acc, plan, source, normalization, loss_kind, loss_from_logits,
+                                      dice_smoothing, normalize_via, autocast_dtype, keep_outputs)
+    finally:
+        if own_streamer is not None:
+            own_streamer.close()
+    stats_dev = acc.finalize(plan.n_b)
+    stats = MiniBatchStats(stats_dev, plan.n_s_mu, acc.max_micro, outputs)
+    return acc.as_gradient_set(), stats
+
+
+def _run_micro_loop(model, acc, plan, source, normalization, loss_kind, loss_from_logits, dice_smoothing,
+                        normalize_via, autocast_dtype, keep_outputs):
+    """The micro loop; K1 records (raw loss, factor, size_k) per micro for the stats."""
+    outputs = []
+    ctx = torch.autocast("cuda", dtype=autocast_dtype) if autocast_dtype is not None else nullcontext()
+    k = -1
+    for k, (xk, yk) in enumerate(source):
+        if k >= plan.n_s_mu:
+            raise AccumulatorOverflowError("source yielded more micro-batches than the plan")
+        factor = normalization_factor(plan, k, normalization)
+        with ctx:
+            out = model(xk)
+            loss = compute_loss(loss_kind, out, yk, from_logits=loss_from_logits, dice_smoothing=dice_smoothing)
+        if normalize_via == "seed":
+            loss.backward(torch.full_like(loss, factor))
+            kscale = 1.0
+        elif normalize_via == "loss_scale":
+            (loss * factor).backward()
+            kscale = 1.0
+        else:
+            loss.backward()
+            kscale = factor
+        acc.add_module_grads(kscale, loss=loss, loss_factor=factor, loss_weight=float(plan.sizes[k]),
+                             last=(k == plan.n_s_mu - 1))
+        if keep_outputs:
+            outputs.append(out.detach())
+    if k + 1 != plan.n_s_mu:
+        raise ValueError(f"source yielded {k + 1} micro-batches, plan expects {plan.n_s_mu}")
+    return outputs
+
+
+def train_mini_batch(model: torch.nn.Module, params: ParameterSet, batch: tuple, plan: MicroBatchPlan,
+                     normalization: str, loss_kind: str, optimizer_state: OptimizerState, *,
+                     loss_from_logits: bool = True, dice_smoothing: float = 1.0, prefetch: bool = False,
+                     accumulator: GradientAccumulator | None = None,
+                     lr_for_step: Callable[[int], float] | None = None, **kw) -> tuple:
+    """Stream micro-batches, then update once (engine.py:233-261)."""
+    x, y = batch
+    total, stats = mini_batch_gradient(model, params, x, y, plan, normalization, loss_kind,
+                                       loss_from_logits=loss_from_logits, dice_smoothing=dice_smoothing,
+                                       prefetch=prefetch, accumulator=accumulator, **kw)
+    if lr_for_step is not None:
+        optimizer_state.lr = lr_for_step(optimizer_state.step_count)
+    apply_update(params, total, optimizer_state)
+    stats.step_count = optimizer_state.step_count
+    return params, stats
+
+
+def train_epoch(model: torch.nn.Module, params: ParameterSet, x, y, *, mini_batch_size: int,
+                micro_batch_size: int | None, normalization: str, loss_kind: str,
+                optimizer_state: OptimizerState, seed: int, epoch_index: int, shuffle: bool = True,
+                loss_from_logits: bool = True, dice_smoothing: float = 1.0, prefetch: bool = False,
+                lr_for_step: Callable[[int], float] | None = None,
+                metric_fn: Callable | None = None, keep_mini_stats: bool = False,
+                accumulator: GradientAccumulator | None = None, staging: Staging | None = None,
+                autocast_dtype: torch.dtype | None = None, streamer: MicroBatchStreamer | None = None,
+                normalize_via: str = "fused") -> EpochStats:
+    """One pass over the dataset in the reference's deterministic shuffled order (engine.py:276-335).
+
+    The whole epoch's micro-batch sequence (mini-batch m = order[m*M:(m+1)*M],
+    each split by ``plan_split``; the last mini-batch may be short and gets its
+    own plan) is streamed as ONE sequence, so the H2D copy of the next
+    mini-batch's first micro-batch overlaps the current mini-batch's tail and
+    optimizer step. ``micro_batch_size=None`` is the no-MBS baseline.
+    """
+    x, y = _as_tensor(x), _as_tensor(y)
+    n = x.shape[0]
+    if n == 0:
+        raise ValueError("dataset is empty")
+    if normalization not in NORMALIZATION_MODES:
+        raise ValueError(f"unknown normalization mode {normalization!r}")
+    order = epoch_order(n, seed, epoch_index, shuffle)
+    on_device = x.device.type == "cuda"
+    if on_device and y.device != x.device:
+        y = y.to(x.device)
+    order_dev = torch.from_numpy(order.astype(np.int64)).to(x.device) if (on_device and shuffle) else None
+    minis, jobs = [], []
+    for start in range(0, n, mini_batch_size):
+        idx = order[start:start + mini_batch_size]
+        n_mu = micro_batch_size if micro_batch_size is not None else len(idx)
+        plan = plan_split(len(idx), n_mu)
+        minis.append((start, idx, plan))
+        for lo, hi in plan.index_ranges:
+            if not shuffle:
+                jobs.append((None, start + lo, hi - lo))
+            elif on_device:
+                jobs.append((order_dev[start + lo:start + hi], 0, hi - lo))
+            else:
+                jobs.append((idx[lo:hi], 0, hi - lo))
+    acc = accumulator if accumulator is not None else GradientAccumulator(params)
+    own_streamer = None
+    if not on_device and streamer is None:
+        max_rows = max(p.n_mu for _, _, p in minis)
+        streamer = own_streamer = make_streamer(x, y, max_rows)
+    model.train()
+    source = iter(_micro_source(x, y, jobs, staging, prefetch, streamer))
+    mini_sizes, all_stats, mini_metrics = [], [], []
+    try:
+        for start, idx, plan in minis:
+            acc.begin(plan.n_s_mu)
+            outputs = _run_micro_loop(model, acc, plan, _take(source, plan.n_s_mu), normalization, loss_kind,
+                                      loss_from_logits, dice_smoothing, normalize_via, autocast_dtype,
+                                      keep_outputs=metric_fn is not None or keep_mini_stats)
+            stats_dev = acc.finalize(plan.n_b)
+            stats = MiniBatchStats(stats_dev, plan.n_s_mu, acc.max_micro, outputs)
+            if lr_for_step is not None:
+                optimizer_state.lr = lr_for_step(optimizer_state.step_count)
+            apply_update(params, acc.as_gradient_set(), optimizer_state)
+            stats.step_count = optimizer_state.step_count
+            mini_sizes.append(len(idx))
+            if metric_fn is not None:
+                yb = y[torch.from_numpy(idx.astype(np.int64)).to(y.device)] if on_device else \
+                    y[torch.from_numpy(idx.astype(np.int64))]
+                mini_metrics.append(float(metric_fn(stats.outputs, yb.to(stats.outputs.device))))
+            if all_stats:
+                all_stats[-1].resolve()  # one mini-batch behind: surfaces NonFiniteError without stalling
+            all_stats.append(stats)
+            if not keep_mini_stats:
+                stats._outputs = []
+    finally:
+        if own_streamer is not None:
+            own_streamer.close()
+    mini_losses = [s.loss for s in all_stats]
+    mean_loss = float(np.dot(mini_losses, mini_sizes) / n)
+    return EpochStats(mini_losses=mini_losses, mean_loss=mean_loss, mini_metrics=mini_metrics,
+                      mini_sizes=mini_sizes, step_count=optimizer_state.step_count,
+                      mini_stats=all_stats if keep_mini_stats else [])
+
+
+def _take(it, n: int):
+    for _ in range(n):
+        try:
+            yield next(it)
+        except StopIteration:
+            return

@@ -1,0 +1,102 @@
+"""Benchmark workloads named by BASELINE.json ``configs`` (synthetic data, random init).
+
+C1 ResNet-18 (10 classes) on CIFAR-shaped 3x32x32, mini 64 / micro 8.
+C2 ResNet-50 (102 classes, Flower-102 shape) 3x224x224, mini 1024 / micro 128.
+C3 U-Net (classic 64..1024, transpose-conv up path, 3 -> 1 channel) 3x384x384
+   with binary masks, mini 256 / micro 48 (ragged tail of 16).
+C5 U-Net 768x768, micro-batch auto-sized to free HBM (memory.fit_micro_batch).
+
+These are the model definitions only; the MBS hot path never depends on them.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+from torch import nn
+
+
+class _DoubleConv(nn.Module):
+    def __init__(self, cin, cout):
+        super().__init__()
+        self.net = nn.Sequential(nn.Conv2d(cin, cout, 3, padding=1, bias=False), nn.BatchNorm2d(cout),
+                                 nn.ReLU(inplace=True), nn.Conv2d(cout, cout, 3, padding=1, bias=False),
+                                 nn.BatchNorm2d(cout), nn.ReLU(inplace=True))
+
+    def forward(self, x):
+        return self.net(x)
+
+
+class _Up(nn.Module):
+    def __init__(self, cin, cout):
+        super().__init__()
+        self.up = nn.ConvTranspose2d(cin, cin // 2, kernel_size=2, stride=2)
+        self.conv = _DoubleConv(cin, cout)
+
+    def forward(self, x, skip):
+        return self.conv(torch.cat([skip, self.up(x)], dim=1))
+
+
+class UNet(nn.Module):
+    """Classic U-Net (Ronneberger et al.), 64->1024 channels, transpose-conv up path."""
+
+    def __init__(self, in_channels: int = 3, out_channels: int = 1):
+        super().__init__()
+        self.inc = _DoubleConv(in_channels, 64)
+        self.downs = nn.ModuleList([_DoubleConv(c, 2 * c) for c in (64, 128, 256, 512)])
+        self.ups = nn.ModuleList([_Up(2 * c, c) for c in (512, 256, 128, 64)])
+        self.pool = nn.MaxPool2d(2)
+        self.outc = nn.Conv2d(64, out_channels, kernel_size=1)
+
+    def forward(self, x):
+        skips = [self.inc(x)]
+        for d in self.downs:
+            skips.append(d(self.pool(skips[-1])))
+        x = skips.pop()
+        for u in self.ups:
+            x = u(x, skips.pop())
+        return self.outc(x)
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    model: str
+    sample_shape: tuple
+    target: str            # "classes" | "mask"
+    n_classes: int
+    mini: int
+    micro: int
+    loss_kind: str
+    optimizer: str         # "sgd" | "adam"
+    normalization: str = "exact_weighted"
+
+
+WORKLOADS = {
+    "c1": Workload("resnet18-cifar-64/8", "resnet18", (3, 32, 32), "classes", 10, 64, 8, "cross_entropy", "sgd"),
+    "c2": Workload("resnet50-224-flower102-1024/128", "resnet50", (3, 224, 224), "classes", 102, 1024, 128,
+                   "cross_entropy", "sgd"),
+    "c3": Workload("unet-384-carvana-256/48", "unet", (3, 384, 384), "mask", 1, 256, 48, "bce_dice", "adam"),
+    "c5": Workload("unet-768-autosized", "unet", (3, 768, 768), "mask", 1, 64, 0, "bce_dice", "adam"),
+}
+
+
+def build_model(w: Workload) -> nn.Module:
+    if w.model in ("resnet18", "resnet50"):
+        import torchvision
+        return getattr(torchvision.models, w.model)(num_classes=w.n_classes)
+    if w.model == "unet":
+        return UNet(w.sample_shape[0], 1)
+    raise ValueError(w.model)
+
+
+def synthetic_data(w: Workload, n: int, seed: int = 0, device="cpu"):
+    """uint8 images (the dataset's natural storage) and int64 labels / float32 {0,1} masks."""
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randint(0, 256, (n,) + w.sample_shape, generator=g, dtype=torch.uint8)
+    if w.target == "classes":
+        y = torch.randint(0, w.n_classes, (n,), generator=g, dtype=torch.int64)
+    else:
+        y = (torch.rand((n, 1) + w.sample_shape[1:], generator=g) < 0.5).float()
+    return x.to(device), y.to(device)

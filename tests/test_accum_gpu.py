@@ -1,0 +1,142 @@
+"""K1 (fused normalise + accumulate + grad norm) vs the fp64 oracle accumulator (engine.py:100-131)."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2110_12484_b200 as mbs
+from oracle import mbs_oracle as O
+from tests.gpu_util import Bag, rel_l2, to64
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(64, 3, 7, 7), (64,), (1,), (3,), (8193,), (257, 129), (5, 5, 3, 3), (100000,), (2048, 1000), (7,)]
+
+
+def _setup(cuda, shapes=SHAPES, channels_last=False):
+    bag = Bag(shapes, cuda, channels_last_4d=channels_last)
+    params = mbs.ParameterSet(bag)
+    return bag, params
+
+
+@pytest.mark.parametrize("mode", ["paper_faithful", "exact_weighted", "off"])
+@pytest.mark.parametrize("n_b,n_mu", [(10, 4), (16, 8), (7, 7), (256, 48)])
+def test_accumulate_matches_oracle(cuda, mode, n_b, n_mu):
+    bag, params = _setup(cuda)
+    acc = mbs.GradientAccumulator(params)
+    plan = mbs.plan_split(n_b, n_mu)
+    oplan = O.plan_split(n_b, n_mu)
+    oacc = O.Accumulator({n: tuple(s) for n, s in zip(params.names(), params.layout.shapes)})
+    acc.begin(plan.n_s_mu)
+    oacc.begin(plan.n_s_mu)
+    g = torch.Generator(device=cuda).manual_seed(n_b * 31 + n_mu)
+    losses = []
+    for k in range(plan.n_s_mu):
+        f = mbs.normalization_factor(plan, k, mode)
+        assert f == O.normalization_factor(oplan, k, mode)
+        grads = [torch.randn(s, device=cuda, generator=g) for s in params.layout.shapes]
+        loss = torch.rand((), device=cuda, generator=g)
+        losses.append(float(loss))
+        acc.add_tensors(grads, f, loss=loss, loss_weight=plan.sizes[k], last=(k == plan.n_s_mu - 1))
+        oacc.add({n: f * to64(t) for n, t in zip(params.names(), grads)})
+    stats = acc.finalize(plan.n_b)
+    sums = acc.sums
+    for n in params.names():
+        assert rel_l2(to64(sums[n]), oacc.sums[n]) <= 1e-6, n
+    flat_ref = np.concatenate([oacc.sums[n].ravel() for n in params.names()])
+    assert rel_l2(to64(torch.cat([sums[n].reshape(-1) for n in params.names()])), flat_ref) <= 1e-6
+    norm2 = float(stats[0])
+    assert np.sqrt(norm2) == pytest.approx(O.l2_norm(oacc.sums), rel=1e-6)
+    assert float(stats[1]) == pytest.approx(O.mini_loss(oplan.sizes, losses, n_b), rel=1e-12)
+    assert float(stats[3]) == plan.n_s_mu
+    assert acc.micro_batches_seen == plan.n_s_mu
+
+
+def test_unit_factor_is_bit_exact(cuda):
+    bag, params = _setup(cuda)
+    acc = mbs.GradientAccumulator(params)
+    acc.begin(3)
+    gs = [[torch.randn(s, device=cuda) for s in params.layout.shapes] for _ in range(3)]
+    for grads in gs:
+        acc.add(dict(zip(params.names(), grads)))
+    for i, n in enumerate(params.names()):
+        want = (gs[0][i] + gs[1][i]) + gs[2][i]   # sequential plan order, fp32
+        assert torch.equal(acc.sums[n], want), n
+
+
+def test_unaligned_and_strided_gradients(cuda):
+    bag, params = _setup(cuda, channels_last=True)
+    acc = mbs.GradientAccumulator(params)
+    acc.begin(2)
+    grads1, grads2 = [], []
+    for s, st in zip(params.layout.shapes, params.layout.strides):
+        base = torch.randn(int(np.prod(s)) + 1, device=cuda)
+        grads1.append(base[1:].as_strided(s, st))            # 4-byte aligned only -> scalar path
+        grads2.append(torch.randn(s, device=cuda))           # NCHW contiguous vs channels_last param
+    acc.add_tensors(grads1, 0.5)
+    acc.add_tensors(grads2, 2.0)
+    for i, n in enumerate(params.names()):
+        want = to64(grads1[i]) * 0.5 + to64(grads2[i]) * 2.0
+        assert rel_l2(to64(acc.sums[n]), want) <= 1e-6, n
+
+
+def test_bucketed_equals_single_call(cuda):
+    bag, params = _setup(cuda)
+    n = len(params.names())
+    a1, a2 = mbs.GradientAccumulator(params), mbs.GradientAccumulator(params)
+    a1.begin(2)
+    a2.begin(2)
+    for k in range(2):
+        grads = [torch.randn(s, device=cuda) for s in params.layout.shapes]
+        a1.add_tensors(grads, 0.25, last=k == 1)
+        # buckets issued in reverse (backward) order
+        for lo, hi in [(7, n), (3, 7), (0, 3)]:
+            a2.add_tensors(grads[lo:hi], 0.25, seg_begin=lo, last=k == 1)
+    assert a1.micro_batches_seen == a2.micro_batches_seen == 2
+    assert torch.equal(a1.flat, a2.flat)
+    s1, s2 = a1.finalize(8), a2.finalize(8)
+    assert float(s1[0]) == float(s2[0])
+
+
+def test_overflow_and_key_errors(cuda):
+    bag, params = _setup(cuda)
+    acc = mbs.GradientAccumulator(params)
+    acc.begin(2)
+    grads = {n: torch.randn(s, device=cuda) for n, s in zip(params.names(), params.layout.shapes)}
+    acc.add(grads)
+    acc.add(grads)
+    with pytest.raises(mbs.AccumulatorOverflowError):      # engine.py:118-121
+        acc.add(grads)
+    acc.begin(2)
+    bad = dict(grads)
+    bad.pop(params.names()[0])
+    with pytest.raises(mbs.AccumulatorOverflowError):      # engine.py:122-125 (key mismatch)
+        acc.add(bad)
+    bad = dict(grads)
+    bad[params.names()[1]] = torch.randn(65, device=cuda)
+    with pytest.raises(mbs.GradientKeyMismatchError):
+        acc.add(bad)
+
+
+def test_begin_zeroes_and_gradient_set_aliases(cuda):
+    bag, params = _setup(cuda)
+    acc = mbs.GradientAccumulator(params)
+    acc.begin(1)
+    grads = {n: torch.randn(s, device=cuda) for n, s in zip(params.names(), params.layout.shapes)}
+    acc.add(grads)
+    total = acc.as_gradient_set()
+    assert torch.equal(total[params.names()[0]], grads[params.names()[0]])
+    acc.begin(1)
+    for n in params.names():          # as_gradient_set aliases the live sums
+        assert float(acc.sums[n].abs().sum()) == 0.0
+        assert float(total[n].abs().sum()) == 0.0
+
+
+def test_nonfinite_is_flagged(cuda):
+    bag, params = _setup(cuda)
+    acc = mbs.GradientAccumulator(params)
+    acc.begin(1)
+    grads = [torch.randn(s, device=cuda) for s in params.layout.shapes]
+    grads[4][17] = float("nan")
+    acc.add_tensors(grads, 1.0, last=True)
+    st = acc.finalize(4)
+    assert float(st[2]) == 1.0
