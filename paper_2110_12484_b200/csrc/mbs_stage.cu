@@ -5,8 +5,8 @@
 // (engine.py:310-312), the contiguous micro slice ascontiguousarray(x[lo:hi])
 // (engine.py:149-151) and the dtype coercion as_array (tensor.py:20-22). The
 // staged bytes are bit-identical to torch's x[rows].to(dtype[, channels_last]):
-// u8 -> f32/bf16/f16 is exact, f32 -> bf16 uses c10's round-to-nearest-even
-// (NaN -> 0x7FC0), f32 -> f16 uses cvt.rn.
+// u8 -> f32/bf16/f16 is exact, f32 -> bf16/f16 use cvt.rn (round-to-nearest-even,
+// canonical NaN), i.e. the conversions torch's CUDA kernels use.
 //
 // The source may be device memory or page-locked host memory (zero-copy over
 // PCIe); 128-bit loads and stores whenever the row base is 16-byte aligned.
@@ -28,11 +28,9 @@ template <> struct Elem<float> { static __device__ __forceinline__ float f(float
 template <> struct Elem<double> { static __device__ __forceinline__ float f(double v) { return __double2float_rn(v); } };
 
 __device__ __forceinline__ uint16_t f32_to_bf16_rne(float f) {
-    // identical to c10::BFloat16 round_to_nearest_even
-    if (f != f) return 0x7FC0u;
-    const uint32_t u = __float_as_uint(f);
-    const uint32_t bias = ((u >> 16) & 1u) + 0x7FFFu;
-    return (uint16_t)((u + bias) >> 16);
+    // cvt.rn.bf16.f32: round-to-nearest-even, canonical NaN 0x7FFF — exactly what
+    // torch's CUDA .to(torch.bfloat16) produces
+    return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
 
 template <int OUT> struct Out;
