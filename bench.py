@@ -117,15 +117,6 @@ def _dist():
 # CPU reference arm (the oracle port: the reference's algorithm in float64)
 # ---------------------------------------------------------------------------
 
-def cpu_reference_step(w, model_cpu, st, x, y, n_b, n_mu):
-    from oracle import mbs_oracle as O
-    from oracle.hybrid import TorchGradFn
-    gf = model_cpu
-    params = gf.params()
-    plan = O.plan_split(n_b, n_mu)
-    O.train_mini_batch(gf, params, x, y, plan, w.normalization, st)
-
-
 def run_cpu_reference(w, steps: int, warmup: int, sample_n_b: int, sample_n_mu: int):
     """Time the float64 CPU oracle on a bounded sample of the workload; returns samples/s."""
     from oracle import mbs_oracle as O
@@ -164,7 +155,7 @@ def main():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=16, help="samples per CPU-reference step")
     args = ap.parse_args()
@@ -212,6 +203,22 @@ def main():
     staging = Staging(dtype=torch.bfloat16, channels_last=True)
     autocast = torch.bfloat16
     n_b, n_mu = w.mini, w.micro
+    autosize = None
+    if n_mu == 0:
+        # config 5: micro-batch auto-sized to free HBM (memory.py:88-101 rule on measured bytes)
+        from paper_2110_12484_b200 import memory
+        from paper_2110_12484_b200.streamer import stage_rows
+
+        def make_batch(k):
+            xb, yb = synthetic_data(w, k, seed=99, device=dev)
+            return stage_rows(xb, xb.dtype, tuple(xb.shape[1:]), None, 0, k, staging, dev), yb
+        budget = memory.measure_budget(model, make_batch, w.loss_kind, optimizer_kind=w.optimizer,
+                                       autocast_dtype=autocast)
+        n_mu = memory.fit_micro_batch(budget)
+        n_b = max(w.mini, 4 * n_mu)          # a mini-batch that cannot fit HBM without streaming
+        autosize = {"capacity_bytes": budget.capacity_bytes, "resident_bytes": budget.resident_bytes,
+                    "data_bytes_per_sample": budget.data_bytes_per_sample, "micro": n_mu, "mini": n_b}
+        torch.cuda.empty_cache()
     plan = mbs.plan_split(n_b, n_mu)
 
     # two mini-batches per rank, alternated every step (> L2: each mini-batch is >= 154 MB of uint8)
@@ -327,7 +334,8 @@ def main():
                        "normalization": w.normalization, "optimizer": w.optimizer,
                        "model_precision": "bf16 autocast on cuDNN/cuBLAS, fp32 master weights; MBS path fp32",
                        "input": "uint8 NCHW staged to bf16 NHWC by K2",
-                       "l2": "inputs > L2: two alternating mini-batches of %.0f MB" % (x_dev[:n_b].numel() / 1e6)},
+                       "l2": "inputs > L2: two alternating mini-batches of %.0f MB" % (x_dev[:n_b].numel() / 1e6),
+                       "autosize": autosize},
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": int(h2d_bytes),
                     "d2h_bytes_per_step": 8 * (4 + 2 * plan.n_s_mu), "ms_per_step": ms_host / args.steps},
             "h2d_overlap_pct": overlap, "h2d_gbs": h2d_gbs, "accum_gbs": k1.get("gbs"),
