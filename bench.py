@@ -189,11 +189,16 @@ def main():
     from paper_2110_12484_b200.streamer import Staging
     from paper_2110_12484_b200.workloads import build_model, synthetic_data
 
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local % max(1, ndev))
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+        torch.cuda.set_device(dev)
+        backend = os.environ.get("MBS_DP_BACKEND", "nccl")   # gloo only for smoke runs of >1 rank per GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(dev)
     torch.backends.cudnn.benchmark = True
     torch.manual_seed(1234 + rank)
@@ -285,7 +290,7 @@ def main():
         return ms, losses
 
     # --- value: inputs resident in HBM ---
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev.index) as clocks:
         ms_dev, _ = timed(False, args.steps, args.warmup, k1_timer=True)
     kstats = TIMER.summary()
     launches_value = TIMER.launches

@@ -14,6 +14,7 @@
 // reduction order so the grad norm is bit-reproducible run to run.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <stdint.h>
 
 #include <algorithm>
@@ -33,15 +34,14 @@ void set_error(const std::string& msg) {
 }
 
 constexpr int kThreads = 256;
-constexpr int kChunk = 8192;       // elements per CTA work unit (K1 / norm)
+constexpr int64_t kMinPerBlock = 4096;   // elements: smallest CTA share (tiny buckets)
+constexpr int64_t kDefaultTile = 8192;   // elements per K1 CTA (MBS_K1_TILE overrides; 0 = balanced)
 constexpr int kMaxPtrs = 1024;     // gradient pointers per K1 launch (kernel-param table)
 constexpr int kUnroll = 4;
 
-struct Chunk {
-    int64_t acc_off;   // element offset into acc
-    int64_t g_off;     // element offset into the segment's gradient tensor
-    int32_t seg;       // segment index
-    int32_t len;       // elements in this chunk (<= kChunk)
+struct Seg {
+    int64_t off;   // element offset of the segment in acc (multiple of 4)
+    int64_t num;   // elements of the segment (its gradient tensor's numel)
 };
 
 struct GradPtrs {
@@ -75,28 +75,30 @@ __device__ __forceinline__ double block_sum(double v, double* smem) {
     return r;  // valid in thread 0 only
 }
 
-// K1: acc[c] = s*g (ASSIGN) or acc[c] += s*g, per chunk; optional ||acc||^2 partial per chunk.
+// Last segment index in [s0, s1) whose offset is <= x (segments sorted, non-overlapping).
+__device__ __forceinline__ int find_seg(const Seg* __restrict__ segs, int s0, int s1, int64_t x) {
+    int a = s0, b = s1 - 1;
+    while (a < b) {
+        const int m = (a + b + 1) >> 1;
+        if (segs[m].off <= x) a = m; else b = m - 1;
+    }
+    return a;
+}
+
+// One contiguous piece of one segment: acc[0..n) (+)= s * g[0..n).
 template <bool ASSIGN, bool NORM>
-__global__ void __launch_bounds__(kThreads)
-k_accum(float* __restrict__ acc, const Chunk* __restrict__ chunks, int64_t chunk0, int seg0,
-        const __grid_constant__ GradPtrs gp, float s, double* __restrict__ partials,
-        const float* __restrict__ loss, double* __restrict__ loss_slot,
-        double* __restrict__ factor_slot, double factor, double* __restrict__ weight_slot, double weight) {
-    __shared__ double red[kThreads / 32];
-    const Chunk c = chunks[chunk0 + blockIdx.x];
-    const float* __restrict__ g = gp.p[c.seg - seg0] + c.g_off;
-    float* __restrict__ a = acc + c.acc_off;
-    double sq = 0.0;
-    int done = 0;
+__device__ __forceinline__ void accum_piece(float* __restrict__ a, const float* __restrict__ g, int64_t n, float s,
+                                            double& sq) {
+    int64_t done = 0;
     if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
-        const int n4 = c.len >> 2;
+        const int64_t n4 = n >> 2;
         const float4* g4 = reinterpret_cast<const float4*>(g);
         float4* a4 = reinterpret_cast<float4*>(a);
-        for (int base = threadIdx.x; base < n4; base += kThreads * kUnroll) {
+        for (int64_t base = threadIdx.x; base < n4; base += kThreads * kUnroll) {
             float4 gv[kUnroll], av[kUnroll];
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
-                const int i = base + u * kThreads;
+                const int64_t i = base + u * kThreads;
                 if (i < n4) {
                     gv[u] = ld_stream(g4 + i);
                     if (!ASSIGN) av[u] = a4[i];
@@ -104,7 +106,7 @@ k_accum(float* __restrict__ acc, const Chunk* __restrict__ chunks, int64_t chunk
             }
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
-                const int i = base + u * kThreads;
+                const int64_t i = base + u * kThreads;
                 if (i < n4) {
                     float4 r;
                     if (ASSIGN) {
@@ -120,14 +122,37 @@ k_accum(float* __restrict__ acc, const Chunk* __restrict__ chunks, int64_t chunk
         }
         done = n4 << 2;
     }
-    for (int i = done + threadIdx.x; i < c.len; i += kThreads) {  // tail / unaligned gradient
+    for (int64_t i = done + threadIdx.x; i < n; i += kThreads) {  // tail / unaligned gradient
         const float r = ASSIGN ? s * g[i] : fmaf(s, g[i], a[i]);
         a[i] = r;
         if (NORM) sq += (double)r * (double)r;
     }
+}
+
+// K1: CTA b owns acc elements [lo0 + b*per_block, +per_block) — a balanced, 128-byte aligned share
+// of the launch's range that may span several segments (small BN/bias tensors) or part of one.
+// acc = s*g (ASSIGN) or acc += s*g; NORM adds this CTA's sum of squares to partials[b].
+template <bool ASSIGN, bool NORM>
+__global__ void __launch_bounds__(kThreads)
+k_accum(float* __restrict__ acc, const Seg* __restrict__ segs, int seg0, int seg1, int64_t lo0, int64_t hi0,
+        int64_t per_block, const __grid_constant__ GradPtrs gp, float s, double* __restrict__ partials,
+        const float* __restrict__ loss, double* __restrict__ loss_slot, double* __restrict__ factor_slot,
+        double factor, double* __restrict__ weight_slot, double weight) {
+    __shared__ double red[kThreads / 32];
+    const int64_t lo = lo0 + (int64_t)blockIdx.x * per_block;
+    const int64_t hi = min(lo + per_block, hi0);
+    double sq = 0.0;
+    if (lo < hi) {
+        for (int si = find_seg(segs, seg0, seg1, lo); si < seg1; ++si) {
+            const Seg sg = segs[si];
+            if (sg.off >= hi) break;
+            const int64_t p0 = max(lo, sg.off), p1 = min(hi, sg.off + sg.num);
+            if (p1 > p0) accum_piece<ASSIGN, NORM>(acc + p0, gp.p[si - seg0] + (p0 - sg.off), p1 - p0, s, sq);
+        }
+    }
     if (NORM) {
         const double t = block_sum<kThreads>(sq, red);
-        if (threadIdx.x == 0) partials[chunk0 + blockIdx.x] = t;
+        if (threadIdx.x == 0) partials[blockIdx.x] = t;
     }
     if (loss != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
         *loss_slot = (double)*loss;
@@ -136,17 +161,19 @@ k_accum(float* __restrict__ acc, const Chunk* __restrict__ chunks, int64_t chunk
     }
 }
 
-// ||acc||^2 partials per chunk (post-all-reduce norm).
+// ||acc||^2 partials over [0, n) (padding is zero), one balanced slice per CTA.
 __global__ void __launch_bounds__(kThreads)
-k_sumsq(const float* __restrict__ acc, const Chunk* __restrict__ chunks, double* __restrict__ partials) {
+k_sumsq(const float* __restrict__ acc, int64_t n, int64_t per_block, double* __restrict__ partials) {
     __shared__ double red[kThreads / 32];
-    const Chunk c = chunks[blockIdx.x];
-    const float* a = acc + c.acc_off;
+    const int64_t lo = (int64_t)blockIdx.x * per_block;
+    const int64_t hi = min(lo + per_block, n);
     double sq = 0.0;
-    const int n4 = c.len >> 2;
-    const float4* a4 = reinterpret_cast<const float4*>(a);
-    for (int i = threadIdx.x; i < n4; i += kThreads) sq += sq4(ld_stream(a4 + i));
-    for (int i = (n4 << 2) + threadIdx.x; i < c.len; i += kThreads) sq += (double)a[i] * (double)a[i];
+    if (lo < hi) {
+        const float4* a4 = reinterpret_cast<const float4*>(acc + lo);
+        const int64_t n4 = (hi - lo) >> 2;
+        for (int64_t i = threadIdx.x; i < n4; i += kThreads) sq += sq4(ld_stream(a4 + i));
+        for (int64_t i = lo + (n4 << 2) + threadIdx.x; i < hi; i += kThreads) sq += (double)acc[i] * (double)acc[i];
+    }
     const double t = block_sum<kThreads>(sq, red);
     if (threadIdx.x == 0) partials[blockIdx.x] = t;
 }
@@ -263,10 +290,12 @@ struct mbs_accum {
     float* acc = nullptr;
     int64_t numel = 0;
     std::vector<int64_t> off, num;
-    std::vector<int64_t> seg_chunk0;   // first chunk of each segment (size nseg+1)
-    Chunk* d_chunks = nullptr;
-    int64_t n_chunks = 0;
-    double* d_partials = nullptr;
+    Seg* d_segs = nullptr;             // device copy of (off, num) per segment
+    int grid = 0;                      // CTAs of a full-range launch (resident CTAs on the device)
+    double* d_partials = nullptr;      // [grid] ||acc||^2 partials, one per CTA of the last NORM launch
+    int n_partials = 0;                // valid partials (0 = stale: finalize recomputes the norm)
+    int64_t tile = kDefaultTile;       // elements per CTA (0 = balanced over resident CTAs)
+    int64_t max_partials = 0;
     double* d_losses = nullptr;        // [max_micro] raw loss per local micro-batch
     double* d_factors = nullptr;       // [max_micro]
     double* d_weights = nullptr;       // [max_micro] sample count of each micro-batch
@@ -343,7 +372,7 @@ int mbs_accum_create(float* acc_dev, int64_t acc_numel, int64_t n_segments,
     h->acc = acc_dev;
     h->numel = acc_numel;
     h->max_micro = max_micro;
-    std::vector<Chunk> chunks;
+    std::vector<Seg> segs;
     int64_t prev_end = 0;
     for (int64_t i = 0; i < n_segments; ++i) {
         const int64_t o = seg_offsets[i], n = seg_numels[i];
@@ -354,22 +383,20 @@ int mbs_accum_create(float* acc_dev, int64_t acc_numel, int64_t n_segments,
         prev_end = o + n;
         h->off.push_back(o);
         h->num.push_back(n);
-        h->seg_chunk0.push_back((int64_t)chunks.size());
-        for (int64_t s = 0; s < n; s += kChunk) {
-            Chunk c;
-            c.acc_off = o + s;
-            c.g_off = s;
-            c.seg = (int32_t)i;
-            c.len = (int32_t)std::min<int64_t>(kChunk, n - s);
-            chunks.push_back(c);
-        }
+        segs.push_back(Seg{o, n});
     }
-    h->seg_chunk0.push_back((int64_t)chunks.size());
-    h->n_chunks = (int64_t)chunks.size();
-    cudaError_t e = cudaMalloc(&h->d_chunks, sizeof(Chunk) * std::max<int64_t>(1, h->n_chunks));
-    if (e == cudaSuccess) e = cudaMemcpy(h->d_chunks, chunks.data(), sizeof(Chunk) * h->n_chunks, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&h->d_partials, sizeof(double) * std::max<int64_t>(1, h->n_chunks));
-    if (e == cudaSuccess) e = cudaMemset(h->d_partials, 0, sizeof(double) * std::max<int64_t>(1, h->n_chunks));
+    // one full-range launch = exactly the resident CTAs of the device: every CTA gets the same
+    // share of elements, so there is no tail wave
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accum<false, true>, kThreads, 0);
+    h->grid = std::max(1, per_sm) * sm_count();
+    if (const char* t = getenv("MBS_K1_TILE")) h->tile = atoll(t);
+    if (h->tile > 0 && h->tile < 1024) h->tile = 1024;
+    h->max_partials = std::max<int64_t>(h->grid, (acc_numel + 1023) / 1024);
+    cudaError_t e = cudaMalloc(&h->d_segs, sizeof(Seg) * segs.size());
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_segs, segs.data(), sizeof(Seg) * segs.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&h->d_partials, sizeof(double) * h->max_partials);
+    if (e == cudaSuccess) e = cudaMemset(h->d_partials, 0, sizeof(double) * h->max_partials);
     if (e == cudaSuccess) e = cudaMalloc(&h->d_losses, sizeof(double) * max_micro * 3);
     if (e == cudaSuccess) e = cudaMemset(h->d_losses, 0, sizeof(double) * max_micro * 3);
     if (e != cudaSuccess) {
@@ -384,7 +411,7 @@ int mbs_accum_create(float* acc_dev, int64_t acc_numel, int64_t n_segments,
 
 int mbs_accum_destroy(mbs_accum_t h) {
     if (!h) return MBS_OK;
-    if (h->d_chunks) cudaFree(h->d_chunks);
+    if (h->d_segs) cudaFree(h->d_segs);
     if (h->d_partials) cudaFree(h->d_partials);
     if (h->d_losses) cudaFree(h->d_losses);
     delete h;
@@ -405,6 +432,7 @@ int mbs_accum_zero(mbs_accum_t h, void* stream) {
     if (!h) return invalid("null accumulator");
     MBS_CK(cudaMemsetAsync(h->acc, 0, sizeof(float) * h->numel, (cudaStream_t)stream));
     h->fresh = false;
+    h->n_partials = 0;
     return MBS_OK;
 }
 
@@ -415,28 +443,45 @@ int mbs_accum_seen(mbs_accum_t h, int64_t* seen, int64_t* expected) {
     return MBS_OK;
 }
 
+// Elements per CTA for a launch over `range` elements: a balanced share for `grid` CTAs,
+// rounded to 128 bytes so every CTA boundary is float4-aligned inside a segment.
+static int64_t share(int64_t range, int grid, int64_t tile) {
+    if (tile > 0) return (tile + 31) / 32 * 32;  // fixed tiles, one CTA each (hardware-balanced)
+    int64_t per = (range + grid - 1) / grid;     // balanced: exactly `grid` CTAs
+    per = std::max<int64_t>(per, kMinPerBlock);
+    return (per + 31) / 32 * 32;
+}
+
 static int launch_accum(mbs_accum_t h, const float* const* grads, int64_t seg_begin, int64_t seg_count,
                         float s, const float* loss_dev, double factor, double weight, bool assign, bool norm,
                         cudaStream_t st) {
     const int64_t slot = h->seen;
+    const int64_t nseg = (int64_t)h->off.size();
+    // the norm partials are only meaningful for a launch covering every segment
+    norm = norm && seg_begin == 0 && seg_count == nseg && seg_count <= kMaxPtrs;
     for (int64_t b = 0; b < seg_count; b += kMaxPtrs) {
         const int64_t cnt = std::min<int64_t>(kMaxPtrs, seg_count - b);
         GradPtrs gp;
         for (int64_t i = 0; i < cnt; ++i) gp.p[i] = grads[b + i];
-        const int64_t s0 = seg_begin + b;
-        const int64_t c0 = h->seg_chunk0[s0], c1 = h->seg_chunk0[s0 + cnt];
-        if (c1 == c0) continue;
+        const int s0 = (int)(seg_begin + b), s1 = (int)(seg_begin + b + cnt);
+        const int64_t lo = h->off[s0], hi = h->off[s1 - 1] + h->num[s1 - 1];
+        if (hi <= lo) continue;
+        const int64_t per = share(hi - lo, h->grid, h->tile);
+        const unsigned grid = (unsigned)((hi - lo + per - 1) / per);
         const float* lp = (b == 0) ? loss_dev : nullptr;
-        dim3 grid((unsigned)(c1 - c0));
+        double* ls = h->d_losses + slot;
+        double* fs = h->d_factors + slot;
+        double* ws = h->d_weights + slot;
         if (assign && norm)
-            k_accum<true, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_chunks, c0, (int)s0, gp, s, h->d_partials, lp, h->d_losses + slot, h->d_factors + slot, factor, h->d_weights + slot, weight);
+            k_accum<true, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
         else if (assign)
-            k_accum<true, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_chunks, c0, (int)s0, gp, s, h->d_partials, lp, h->d_losses + slot, h->d_factors + slot, factor, h->d_weights + slot, weight);
+            k_accum<true, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
         else if (norm)
-            k_accum<false, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_chunks, c0, (int)s0, gp, s, h->d_partials, lp, h->d_losses + slot, h->d_factors + slot, factor, h->d_weights + slot, weight);
+            k_accum<false, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
         else
-            k_accum<false, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_chunks, c0, (int)s0, gp, s, h->d_partials, lp, h->d_losses + slot, h->d_factors + slot, factor, h->d_weights + slot, weight);
+            k_accum<false, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
         MBS_CK_LAUNCH("k_accum");
+        h->n_partials = norm ? (int)grid : 0;
     }
     return MBS_OK;
 }
@@ -494,15 +539,21 @@ int mbs_accum_add_flat(mbs_accum_t h, const float* g_flat, double factor, const 
 
 int mbs_accum_norm(mbs_accum_t h, void* stream) {
     if (!h) return invalid("null accumulator");
-    if (h->n_chunks == 0) return MBS_OK;
-    k_sumsq<<<(unsigned)h->n_chunks, kThreads, 0, (cudaStream_t)stream>>>(h->acc, h->d_chunks, h->d_partials);
+    const int64_t per = share(h->numel, h->grid, 0);
+    const unsigned grid = (unsigned)((h->numel + per - 1) / per);
+    k_sumsq<<<grid, kThreads, 0, (cudaStream_t)stream>>>(h->acc, h->numel, per, h->d_partials);
     MBS_CK_LAUNCH("k_sumsq");
+    h->n_partials = (int)grid;
     return MBS_OK;
 }
 
 int mbs_accum_finalize(mbs_accum_t h, int64_t n_b, double* stats_dev, void* stream) {
     if (!h || !stats_dev || n_b < 1) return invalid("mbs_accum_finalize: null handle/stats or n_b < 1");
-    k_finalize<<<1, 1024, 0, (cudaStream_t)stream>>>(h->d_partials, h->n_chunks, h->d_losses, h->d_factors,
+    if (h->n_partials == 0) {  // no fused norm since the last change of acc: compute it now
+        int st = mbs_accum_norm(h, stream);
+        if (st) return st;
+    }
+    k_finalize<<<1, 1024, 0, (cudaStream_t)stream>>>(h->d_partials, h->n_partials, h->d_losses, h->d_factors,
                                                     h->d_weights, h->seen, h->max_micro, n_b, stats_dev);
     MBS_CK_LAUNCH("k_finalize");
     return MBS_OK;

@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "mbs_common.h"
 
 namespace mbs {
@@ -146,6 +148,64 @@ k_stage_nhwc(const TI* __restrict__ src, const int64_t* __restrict__ rows, int64
     }
 }
 
+// Fully vectorised path (every row a whole number of kPix units, 16-byte aligned): a
+// grid-stride loop over (row, unit) with two units in flight per thread, grid = resident CTAs.
+template <typename TI, int OUT, int C, bool NHWC>
+__global__ void __launch_bounds__(kStageThreads)
+k_stage_vec(const TI* __restrict__ src, const int64_t* __restrict__ rows, int64_t row0, int64_t HW,
+            int64_t upr, int64_t total, typename Out<OUT>::T* __restrict__ dst) {
+    using TO = typename Out<OUT>::T;
+    const int64_t stride = (int64_t)gridDim.x * kStageThreads;
+    for (int64_t u0 = (int64_t)blockIdx.x * kStageThreads + threadIdx.x; u0 < total; u0 += 2 * stride) {
+        float v[2][C][kPix];
+        int64_t r[2], p[2];
+        bool ok[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int64_t u = u0 + j * stride;
+            ok[j] = u < total;
+            r[j] = ok[j] ? u / upr : 0;
+            p[j] = ok[j] ? (u - r[j] * upr) * kPix : 0;
+            if (ok[j]) {
+                const TI* s = src + src_row(rows, row0, r[j]) * (int64_t)C * HW + p[j];
+#pragma unroll
+                for (int c = 0; c < C; ++c) load_pix<TI>(s + c * HW, v[j][c], true);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            if (!ok[j]) continue;
+            if (NHWC) {
+                TO o[kPix * C];
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+#pragma unroll
+                    for (int i = 0; i < kPix; ++i) o[i * C + c] = Out<OUT>::cvt(v[j][c][i]);
+                store_vec<TO>(dst + (r[j] * HW + p[j]) * C, o, kPix * C, true);
+            } else {
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    TO o[kPix];
+#pragma unroll
+                    for (int i = 0; i < kPix; ++i) o[i] = Out<OUT>::cvt(v[j][c][i]);
+                    store_vec<TO>(dst + (r[j] * C + c) * HW + p[j], o, kPix, true);
+                }
+            }
+        }
+    }
+}
+
+static int resident_grid(int64_t units) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
+    const int64_t want = (units + kStageThreads - 1) / kStageThreads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * (2048 / kStageThreads)));
+}
+
 // Generic NHWC for any C (scalar; one thread per output element).
 template <typename TI, int OUT>
 __global__ void __launch_bounds__(kStageThreads)
@@ -178,6 +238,30 @@ static int stage_typed(const void* src, const int64_t* rows, int64_t row0, int64
     auto* d = static_cast<TO*>(dst);
     const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
     if (n_rows > 65535) return invalid("mbs_stage: at most 65535 rows per call");
+    {
+        // fully vectorised grid-stride path: whole kPix units per channel plane, 16-byte aligned
+        const bool nhwc = layout == MBS_NHWC && C > 1;
+        const bool plane_ok = (HW % kPix == 0) && ((HW * (int64_t)sizeof(TI)) % 16 == 0) && (sa % 16 == 0) &&
+                              (da % 16 == 0) && ((kPix * sizeof(TO)) % 16 == 0);
+        if (plane_ok && (layout == MBS_NCHW || layout == MBS_NHWC) && C >= 1 && C <= 4) {
+            const int64_t upr = HW / kPix, total = n_rows * upr;
+            const int grid = resident_grid((total + 1) / 2);
+#define MBS_STAGE_VEC(CC)                                                                                   \
+    do {                                                                                                    \
+        if (nhwc) k_stage_vec<TI, OUT, CC, true><<<grid, kStageThreads, 0, st>>>(s, rows, row0, HW, upr, total, d); \
+        else k_stage_vec<TI, OUT, CC, false><<<grid, kStageThreads, 0, st>>>(s, rows, row0, HW, upr, total, d);     \
+    } while (0)
+            switch (C) {
+                case 1: MBS_STAGE_VEC(1); break;
+                case 2: MBS_STAGE_VEC(2); break;
+                case 3: MBS_STAGE_VEC(3); break;
+                default: MBS_STAGE_VEC(4); break;
+            }
+#undef MBS_STAGE_VEC
+            MBS_CK_LAUNCH("k_stage_vec");
+            return MBS_OK;
+        }
+    }
     if (layout == MBS_NCHW || C == 1) {
         // vector path needs 16-byte aligned rows in both src and dst
         const bool vec = (sa % 16 == 0) && (da % 16 == 0) && ((E * (int64_t)sizeof(TI)) % 16 == 0) &&

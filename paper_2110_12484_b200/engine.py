@@ -141,6 +141,7 @@ class GradientAccumulator:
         self._h = h
         self._views = self.layout.views(self.flat)
         self._plist = [params[n] for n in self.layout.names]
+        self._ptr_table = (ctypes.c_void_p * len(self._plist))()
         self._pending_zero = False
         self._fresh = True
         self._covered = 0
@@ -204,9 +205,18 @@ class GradientAccumulator:
             N.check(N.lib().mbs_accum_zero(self._h, _stream_ptr()), "mbs_accum_zero")
         self._pending_zero = False
 
+    def _same_memory_order(self, g: torch.Tensor, i: int) -> bool:
+        """Dense tensors of one shape share their memory order iff strides agree on every dim of size > 1
+        (autograd's layout contract ignores size-1 dims, e.g. 1x1 conv weights in channels_last)."""
+        shape, stride = self.layout.shapes[i], self.layout.strides[i]
+        if tuple(g.shape) != shape or any(a != b for a, b, n in zip(g.stride(), stride, shape) if n > 1):
+            return False
+        return sum((n - 1) * st for n, st in zip(shape, g.stride())) == g.numel() - 1   # dense, no overlap
+
     def _conform(self, g: torch.Tensor, i: int) -> torch.Tensor:
         shape, stride = self.layout.shapes[i], self.layout.strides[i]
-        if g.dtype == torch.float32 and g.device == self.flat.device and tuple(g.stride()) == stride:
+        if g.dtype == torch.float32 and g.device == self.flat.device and (
+                tuple(g.stride()) == stride or self._same_memory_order(g, i)):
             return g
         out = torch.empty_strided(shape, stride, dtype=torch.float32, device=self.flat.device)
         out.copy_(g)
@@ -246,15 +256,40 @@ class GradientAccumulator:
     def add_module_grads(self, factor: float, *, loss: torch.Tensor | None = None,
                          loss_factor: float | None = None, loss_weight: float = 0.0, last: bool = False,
                          stream=None) -> None:
-        """K1 straight from the module's ``.grad`` tensors, which are then released."""
-        grads = []
-        for p in self._plist:
-            if p.grad is None:
+        """K1 straight from the module's ``.grad`` tensors, which are then released.
+
+        Hot path: the pointer table is a preallocated ctypes array; a gradient
+        is only re-laid-out when its dtype/strides differ from the parameter's.
+        """
+        ptrs = self._ptr_table
+        keep = []
+        strides = self.layout.strides
+        for j, p in enumerate(self._plist):
+            g = p.grad
+            if g is None:
                 raise AccumulatorOverflowError("gradient keys do not match accumulator parameters "
                                                "(a parameter received no gradient)")
-            grads.append(p.grad)
-        self.add_tensors(grads, factor, loss=loss, loss_factor=loss_factor, loss_weight=loss_weight, last=last,
-                         stream=stream)
+            if g.dtype is not torch.float32 or (g.stride() != strides[j] and not self._same_memory_order(g, j)):
+                g = self._conform(g, j)
+                keep.append(g)
+            ptrs[j] = g.data_ptr()
+        lp = None
+        if loss is not None:
+            loss = loss.detach()
+            if loss.dtype != torch.float32:
+                loss = loss.float()
+            keep.append(loss)
+            lp = loss.data_ptr()
+        lf = float(factor if loss_factor is None else loss_factor)
+        n = len(self._plist)
+        t0 = TIMER.start(stream)
+        N.check(N.lib().mbs_accum_add(self._h, ptrs, 0, n, float(factor), lp, lf, float(loss_weight),
+                                      int(bool(last)), _stream_ptr(stream)), "mbs_accum_add")
+        if t0 is not None:
+            TIMER.stop("k1_accumulate", t0, (8 if self._fresh else 12) * self.layout.n_params, stream)
+        self._fresh = False
+        self._covered = 0
+        self._pending_zero = False
         for p in self._plist:
             p.grad = None
 

@@ -140,3 +140,20 @@ def test_nonfinite_is_flagged(cuda):
     acc.add_tensors(grads, 1.0, last=True)
     st = acc.finalize(4)
     assert float(st[2]) == 1.0
+
+
+def test_size1_dim_strides_are_not_copied(cuda):
+    """1x1 conv weights in channels_last: autograd's grad strides differ only on size-1 dims."""
+    conv = torch.nn.Conv2d(64, 256, 1).to(cuda).to(memory_format=torch.channels_last)
+    params = mbs.ParameterSet(conv)
+    acc = mbs.GradientAccumulator(params)
+    w = params.names()[0]
+    g = torch.randn(256, 64, 1, 1, device=cuda)               # strides (64, 1, 1, 1)
+    assert g.stride() != params.layout.strides[0]
+    assert acc._same_memory_order(g, 0)
+    assert acc._conform(g, 0) is g
+    acc.begin(1)
+    acc.add({w: g, params.names()[1]: torch.ones(256, device=cuda)})
+    assert torch.equal(acc.sums[w], g)
+    assert not acc._same_memory_order(torch.randn(256, 64, 1, 1, device=cuda).transpose(0, 1).reshape(
+        256, 64, 1, 1)[:, :, :, :].as_strided((256, 64, 1, 1), (1, 256, 1, 1)), 0)
