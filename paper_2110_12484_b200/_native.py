@@ -14,7 +14,7 @@ from ctypes import POINTER, c_double, c_int, c_int64, c_void_p
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmbs_native.so")
+LIB_PATH = os.environ.get("MBS_NATIVE_LIB") or os.path.join(_HERE, "libmbs_native.so")  # override: kernel A/B runs
 
 # status codes (include/mbs.h)
 OK, EINVAL, EOVERFLOW, EKEY, ECUDA, ENONFINITE = range(6)

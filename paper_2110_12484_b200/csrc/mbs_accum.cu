@@ -37,7 +37,13 @@ constexpr int kThreads = 256;
 constexpr int64_t kMinPerBlock = 4096;   // elements: smallest CTA share (tiny buckets)
 constexpr int64_t kDefaultTile = 8192;   // elements per K1 CTA (MBS_K1_TILE overrides; 0 = balanced)
 constexpr int kMaxPtrs = 1024;     // gradient pointers per K1 launch (kernel-param table)
-constexpr int kUnroll = 4;
+#ifndef MBS_K1_UNROLL
+#define MBS_K1_UNROLL 4
+#endif
+#ifndef MBS_K1_MINBLOCKS
+#define MBS_K1_MINBLOCKS 1
+#endif
+constexpr int kUnroll = MBS_K1_UNROLL;
 
 struct Seg {
     int64_t off;   // element offset of the segment in acc (multiple of 4)
@@ -133,7 +139,7 @@ __device__ __forceinline__ void accum_piece(float* __restrict__ a, const float* 
 // of the launch's range that may span several segments (small BN/bias tensors) or part of one.
 // acc = s*g (ASSIGN) or acc += s*g; NORM adds this CTA's sum of squares to partials[b].
 template <bool ASSIGN, bool NORM>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, MBS_K1_MINBLOCKS)
 k_accum(float* __restrict__ acc, const Seg* __restrict__ segs, int seg0, int seg1, int64_t lo0, int64_t hi0,
         int64_t per_block, const __grid_constant__ GradPtrs gp, float s, double* __restrict__ partials,
         const float* __restrict__ loss, double* __restrict__ loss_slot, double* __restrict__ factor_slot,
@@ -212,27 +218,47 @@ __device__ __forceinline__ bool guard_tripped(const double* guard) {
     return guard != nullptr && !isfinite(*guard);
 }
 
-// K3a: optim.py:52-65 — g' = g + wd*w; v = mu*v + g'; w -= lr*v.
+// K3a: optim.py:52-65 — g' = g + wd*w; v = mu*v + g'; w -= lr*v. Two float4s per thread per
+// iteration (6 independent 16-byte loads in flight).
+template <bool READ_V, bool WD>
+__device__ __forceinline__ void sgd4(float4& ww, float4& vv, const float4 gg, float lr, float mu, float wd) {
+    const float gx = WD ? fmaf(wd, ww.x, gg.x) : gg.x;
+    const float gy = WD ? fmaf(wd, ww.y, gg.y) : gg.y;
+    const float gz = WD ? fmaf(wd, ww.z, gg.z) : gg.z;
+    const float gw = WD ? fmaf(wd, ww.w, gg.w) : gg.w;
+    if (!READ_V) vv = make_float4(0.f, 0.f, 0.f, 0.f);
+    vv.x = fmaf(mu, vv.x, gx); vv.y = fmaf(mu, vv.y, gy);
+    vv.z = fmaf(mu, vv.z, gz); vv.w = fmaf(mu, vv.w, gw);
+    ww.x = fmaf(-lr, vv.x, ww.x); ww.y = fmaf(-lr, vv.y, ww.y);
+    ww.z = fmaf(-lr, vv.z, ww.z); ww.w = fmaf(-lr, vv.w, ww.w);
+}
+
 template <bool READ_V, bool WD>
 __global__ void __launch_bounds__(kThreads)
 k_sgd(float4* __restrict__ w, const float4* __restrict__ g, float4* __restrict__ v, int64_t n4,
       float lr, float mu, float wd, const double* __restrict__ guard) {
     if (guard_tripped(guard)) return;
     const int64_t stride = (int64_t)gridDim.x * kThreads;
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n4; i += stride) {
-        const float4 gg = ld_stream(g + i);
-        float4 ww = w[i];
-        float4 vv = READ_V ? v[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float gx = WD ? fmaf(wd, ww.x, gg.x) : gg.x;
-        float gy = WD ? fmaf(wd, ww.y, gg.y) : gg.y;
-        float gz = WD ? fmaf(wd, ww.z, gg.z) : gg.z;
-        float gw = WD ? fmaf(wd, ww.w, gg.w) : gg.w;
-        vv.x = fmaf(mu, vv.x, gx); vv.y = fmaf(mu, vv.y, gy);
-        vv.z = fmaf(mu, vv.z, gz); vv.w = fmaf(mu, vv.w, gw);
-        ww.x = fmaf(-lr, vv.x, ww.x); ww.y = fmaf(-lr, vv.y, ww.y);
-        ww.z = fmaf(-lr, vv.z, ww.z); ww.w = fmaf(-lr, vv.w, ww.w);
-        v[i] = vv;
-        w[i] = ww;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n4; i += 2 * stride) {
+        const int64_t i2 = i + stride;
+        const bool two = i2 < n4;
+        const float4 g0 = ld_stream(g + i);
+        float4 w0 = w[i];
+        float4 v0 = READ_V ? v[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 g1, w1, v1;
+        if (two) {
+            g1 = ld_stream(g + i2);
+            w1 = w[i2];
+            v1 = READ_V ? v[i2] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        sgd4<READ_V, WD>(w0, v0, g0, lr, mu, wd);
+        v[i] = v0;
+        w[i] = w0;
+        if (two) {
+            sgd4<READ_V, WD>(w1, v1, g1, lr, mu, wd);
+            v[i2] = v1;
+            w[i2] = w1;
+        }
     }
 }
 
@@ -247,7 +273,15 @@ __device__ __forceinline__ void adam1(float& w, float& m, float& v, float g, flo
     w = w - __fdiv_rn(lr * mh, vh + eps);
 }
 
-// K3b: optim.py:68-93 — bias-corrected Adam, coupled weight decay.
+// K3b: optim.py:68-93 — bias-corrected Adam, coupled weight decay; two float4s per iteration.
+__device__ __forceinline__ void adam4(float4& ww, float4& mm, float4& vv, const float4 gg, float lr, float b1,
+                                      float omb1, float b2, float omb2, float c1, float c2, float eps, float wd) {
+    adam1(ww.x, mm.x, vv.x, gg.x, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
+    adam1(ww.y, mm.y, vv.y, gg.y, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
+    adam1(ww.z, mm.z, vv.z, gg.z, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
+    adam1(ww.w, mm.w, vv.w, gg.w, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
+}
+
 __global__ void __launch_bounds__(kThreads)
 k_adam(float4* __restrict__ w, const float4* __restrict__ g, float4* __restrict__ m,
        float4* __restrict__ v, int64_t n4, float lr, float b1, float b2, float c1, float c2,
@@ -255,14 +289,22 @@ k_adam(float4* __restrict__ w, const float4* __restrict__ g, float4* __restrict_
     if (guard_tripped(guard)) return;
     const float omb1 = 1.f - b1, omb2 = 1.f - b2;
     const int64_t stride = (int64_t)gridDim.x * kThreads;
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n4; i += stride) {
-        const float4 gg = ld_stream(g + i);
-        float4 ww = w[i], mm = m[i], vv = v[i];
-        adam1(ww.x, mm.x, vv.x, gg.x, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
-        adam1(ww.y, mm.y, vv.y, gg.y, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
-        adam1(ww.z, mm.z, vv.z, gg.z, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
-        adam1(ww.w, mm.w, vv.w, gg.w, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
-        w[i] = ww; m[i] = mm; v[i] = vv;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n4; i += 2 * stride) {
+        const int64_t i2 = i + stride;
+        const bool two = i2 < n4;
+        const float4 g0 = ld_stream(g + i);
+        float4 w0 = w[i], m0 = m[i], v0 = v[i];
+        float4 g1, w1, m1, v1;
+        if (two) {
+            g1 = ld_stream(g + i2);
+            w1 = w[i2]; m1 = m[i2]; v1 = v[i2];
+        }
+        adam4(w0, m0, v0, g0, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
+        w[i] = w0; m[i] = m0; v[i] = v0;
+        if (two) {
+            adam4(w1, m1, v1, g1, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
+            w[i2] = w1; m[i2] = m1; v[i2] = v1;
+        }
     }
 }
 

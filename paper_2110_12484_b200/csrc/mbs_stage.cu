@@ -150,18 +150,34 @@ k_stage_nhwc(const TI* __restrict__ src, const int64_t* __restrict__ rows, int64
 
 // Fully vectorised path (every row a whole number of kPix units, 16-byte aligned): a
 // grid-stride loop over (row, unit) with two units in flight per thread, grid = resident CTAs.
+// The loads are kept as raw 16-byte vectors (4 registers each) until the conversion at store
+// time, so the kernel stays at ~40 registers and keeps all 8 CTAs/SM resident.
+template <typename TI>
+__device__ __forceinline__ float raw_elem(const uint4* raw, int i) {
+    if constexpr (sizeof(TI) == 1) {
+        const uint32_t w = reinterpret_cast<const uint32_t*>(raw)[i >> 2];
+        return (float)((w >> ((i & 3) * 8)) & 0xFFu);
+    } else if constexpr (sizeof(TI) == 4) {
+        return reinterpret_cast<const float*>(raw)[i];
+    } else {
+        return __double2float_rn(reinterpret_cast<const double*>(raw)[i]);
+    }
+}
+
 template <typename TI, int OUT, int C, bool NHWC>
 __global__ void __launch_bounds__(kStageThreads)
 k_stage_vec(const TI* __restrict__ src, const int64_t* __restrict__ rows, int64_t row0, int64_t HW,
             int64_t upr, int64_t total, typename Out<OUT>::T* __restrict__ dst) {
     using TO = typename Out<OUT>::T;
+    constexpr int NV = kPix * (int)sizeof(TI) / 16;   // 16-byte vectors per channel unit
+    constexpr int UN = sizeof(TI) == 1 ? 2 : 1;        // units in flight per thread (register budget)
     const int64_t stride = (int64_t)gridDim.x * kStageThreads;
-    for (int64_t u0 = (int64_t)blockIdx.x * kStageThreads + threadIdx.x; u0 < total; u0 += 2 * stride) {
-        float v[2][C][kPix];
-        int64_t r[2], p[2];
-        bool ok[2];
+    for (int64_t u0 = (int64_t)blockIdx.x * kStageThreads + threadIdx.x; u0 < total; u0 += UN * stride) {
+        uint4 raw[UN][C][NV];
+        int64_t r[UN], p[UN];
+        bool ok[UN];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < UN; ++j) {
             const int64_t u = u0 + j * stride;
             ok[j] = u < total;
             r[j] = ok[j] ? u / upr : 0;
@@ -169,26 +185,43 @@ k_stage_vec(const TI* __restrict__ src, const int64_t* __restrict__ rows, int64_
             if (ok[j]) {
                 const TI* s = src + src_row(rows, row0, r[j]) * (int64_t)C * HW + p[j];
 #pragma unroll
-                for (int c = 0; c < C; ++c) load_pix<TI>(s + c * HW, v[j][c], true);
+                for (int c = 0; c < C; ++c)
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) raw[j][c][v] = reinterpret_cast<const uint4*>(s + c * HW)[v];
             }
         }
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < UN; ++j) {
             if (!ok[j]) continue;
             if (NHWC) {
-                TO o[kPix * C];
+                TO* d = dst + (r[j] * HW + p[j]) * C;
+                constexpr int per = 16 / (int)sizeof(TO);          // outputs per 16-byte store
 #pragma unroll
-                for (int c = 0; c < C; ++c)
+                for (int q = 0; q < kPix * C / per; ++q) {
+                    TO o[per];
 #pragma unroll
-                    for (int i = 0; i < kPix; ++i) o[i * C + c] = Out<OUT>::cvt(v[j][c][i]);
-                store_vec<TO>(dst + (r[j] * HW + p[j]) * C, o, kPix * C, true);
+                    for (int e = 0; e < per; ++e) {
+                        const int k = q * per + e;                 // interleaved index: pixel k / C, channel k % C
+                        o[e] = Out<OUT>::cvt(raw_elem<TI>(raw[j][k % C], k / C));
+                    }
+                    uint4 w;
+                    memcpy(&w, o, 16);
+                    reinterpret_cast<uint4*>(d)[q] = w;
+                }
             } else {
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
-                    TO o[kPix];
+                    TO* d = dst + (r[j] * C + c) * HW + p[j];
+                    constexpr int per = 16 / (int)sizeof(TO);
 #pragma unroll
-                    for (int i = 0; i < kPix; ++i) o[i] = Out<OUT>::cvt(v[j][c][i]);
-                    store_vec<TO>(dst + (r[j] * C + c) * HW + p[j], o, kPix, true);
+                    for (int q = 0; q < kPix / per; ++q) {
+                        TO o[per];
+#pragma unroll
+                        for (int e = 0; e < per; ++e) o[e] = Out<OUT>::cvt(raw_elem<TI>(raw[j][c], q * per + e));
+                        uint4 w;
+                        memcpy(&w, o, 16);
+                        reinterpret_cast<uint4*>(d)[q] = w;
+                    }
                 }
             }
         }
