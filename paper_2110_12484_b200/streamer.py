@@ -146,8 +146,8 @@ class MicroBatchStreamer:
         self._h = h
         self.dev_slots = [torch.empty(self.slot_bytes, dtype=torch.uint8, device=self.device)
                           for _ in range(self.n_slots)]
-        self.jobs_issued: list = []   # (job_seq, n_rows) for timing collection
-        self._timings: dict = {}
+        self.jobs_issued: list = []   # (job_seq, n_rows) not yet harvested
+        self._harvested: list = []    # (gather_ms, copy_ms, blocked_ms, bytes) of older jobs
 
     def close(self):
         if getattr(self, "_h", None):
@@ -177,6 +177,9 @@ class MicroBatchStreamer:
         N.check(N.lib().mbs_streamer_submit(self._h, slot, parts, 2, rows_ptr, int(row0), int(n),
                                             ctypes.byref(job)), "mbs_streamer_submit")
         self.jobs_issued.append((job.value, n))
+        if len(self.jobs_issued) > 128:       # harvest long-finished jobs before the native ring (256) wraps
+            old, self.jobs_issued = self.jobs_issued[:64], self.jobs_issued[64:]
+            self._harvested.extend(self._read_timings(old))
 
     def stream(self, x: torch.Tensor, y: torch.Tensor, jobs, staging: Staging | None, *, prefetch: bool = True):
         """Yield (xk, yk) device tensors for each (rows, row0, n) job over host tensors x, y."""
@@ -213,14 +216,19 @@ class MicroBatchStreamer:
 
     def timings(self, flush: bool = True) -> list:
         """Per-job (gather_ms, copy_ms, blocked_ms, bytes) for the jobs issued so far (synchronises)."""
+        out = self._harvested + self._read_timings(self.jobs_issued)
+        if flush:
+            self.jobs_issued = []
+            self._harvested = []
+        return out
+
+    def _read_timings(self, jobs) -> list:
         out = []
-        for seq, _n in self.jobs_issued:
+        for seq, _n in jobs:
             g, c, b = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
             nb = ctypes.c_int64()
             st = N.lib().mbs_streamer_timing(self._h, seq, ctypes.byref(g), ctypes.byref(c), ctypes.byref(b),
                                              ctypes.byref(nb))
             if st == N.OK:
                 out.append((g.value, c.value, b.value, nb.value))
-        if flush:
-            self.jobs_issued = []
         return out

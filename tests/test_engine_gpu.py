@@ -182,3 +182,45 @@ def test_step_count_is_per_mini_batch(cuda):
     es = mbs.train_epoch(mod, params, x, y, mini_batch_size=7, micro_batch_size=2, normalization="paper_faithful",
                          loss_kind="mse", optimizer_state=st, seed=1, epoch_index=0)
     assert es.step_count == 4 and es.mini_sizes == [7, 7, 7, 3]   # never per micro-batch (SPEC acceptance 6)
+
+
+def test_edge_cases(cuda):
+    meta = load_json("e2e.json")["mlp_mse"]
+    a = load_npz("e2e.npz")
+    mod, params = _model(meta, a, "mlp_mse", cuda)
+    st = mbs.adam_state()
+    with pytest.raises(ValueError):                               # engine.py:295-296
+        mbs.train_epoch(mod, params, torch.zeros(0, 6, device=cuda), torch.zeros(0, 3, device=cuda),
+                        mini_batch_size=4, micro_batch_size=2, normalization="off", loss_kind="mse",
+                        optimizer_state=st, seed=0, epoch_index=0)
+    x, y = _xy(a, "mlp_mse", meta, 0, 5, cuda)
+    with pytest.raises(ValueError):                               # engine.py:197-198
+        mbs.mini_batch_gradient(mod, params, x, y, mbs.plan_split(6, 2), "off", "mse")
+    with pytest.raises(ValueError):
+        mbs.mini_batch_gradient(mod, params, x, y, mbs.plan_split(5, 2), "bogus", "mse")
+    with pytest.raises(ValueError):
+        mbs.mini_batch_gradient(mod, params, x, y, mbs.plan_split(5, 2), "off", "mse", normalize_via="x")
+    # n_mu > n_b clamps (engine.py:66-67); size-1 micro-batches are legal
+    total, s = mbs.mini_batch_gradient(mod, params, x, y, mbs.plan_split(5, 8), "paper_faithful", "mse")
+    assert s.n_micro == 1
+    total1, s1 = mbs.mini_batch_gradient(mod, params, x, y, mbs.plan_split(5, 1), "exact_weighted", "mse")
+    assert s1.n_micro == 5
+    assert rel_l2(total1.flat.double().cpu().numpy(), total.flat.double().cpu().numpy()) <= 1e-6
+    # N_smu = 1: identical to plain mini-batch training in every mode
+    outs = [mbs.mini_batch_gradient(mod, params, x, y, mbs.plan_split(5, 5), m, "mse")[0].flat.clone()
+            for m in ("paper_faithful", "exact_weighted", "off")]
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+def test_nonfinite_loss_raises_and_keeps_params(cuda):
+    meta = load_json("e2e.json")["mlp_mse"]
+    a = load_npz("e2e.npz")
+    mod, params = _model(meta, a, "mlp_mse", cuda)
+    x, y = _xy(a, "mlp_mse", meta, 0, 6, cuda)
+    x[2, 0] = float("inf")
+    before = params.flat.clone()
+    st = mbs.sgd_state()
+    _, stats = mbs.train_mini_batch(mod, params, (x, y), mbs.plan_split(6, 3), "paper_faithful", "mse", st)
+    with pytest.raises(mbs.NonFiniteError):
+        stats.loss
+    assert torch.equal(params.flat, before)          # the device guard skipped the step
