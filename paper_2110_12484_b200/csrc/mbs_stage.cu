@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "mbs_common.h"
@@ -228,6 +230,58 @@ k_stage_vec(const TI* __restrict__ src, const int64_t* __restrict__ rows, int64_
     }
 }
 
+// NCHW -> NHWC through shared memory: a CTA converts a tile of kTilePx pixels x C channels
+// (coalesced 16-byte plane loads), writes it NHWC-interleaved into smem, then the whole tile
+// leaves with fully coalesced 16-byte stores (lane i writes bytes [16i, 16i+16) of the tile).
+constexpr int kTilePx = kStageThreads * kPix;   // 4096 pixels per CTA tile
+
+template <typename TI, int OUT, int C>
+__global__ void __launch_bounds__(kStageThreads)
+k_stage_nhwc_smem(const TI* __restrict__ src, const int64_t* __restrict__ rows, int64_t row0, int64_t HW,
+                  int64_t tiles_per_row, int64_t total_tiles, typename Out<OUT>::T* __restrict__ dst) {
+    using TO = typename Out<OUT>::T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TO* tile = reinterpret_cast<TO*>(smem_raw);
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const int64_t r = t / tiles_per_row;
+        const int64_t p0 = (t - r * tiles_per_row) * kTilePx;
+        const int64_t npx = min((int64_t)kTilePx, HW - p0);
+        const TI* s = src + src_row(rows, row0, r) * (int64_t)C * HW + p0;
+        const int q0 = threadIdx.x * kPix;
+        if (q0 + kPix <= npx) {
+            float v[C][kPix];
+#pragma unroll
+            for (int c = 0; c < C; ++c) load_pix<TI>(s + c * HW + q0, v[c], true);
+            TO o[kPix * C];
+#pragma unroll
+            for (int i = 0; i < kPix; ++i)
+#pragma unroll
+                for (int c = 0; c < C; ++c) o[i * C + c] = Out<OUT>::cvt(v[c][i]);
+            store_vec<TO>(tile + (int64_t)q0 * C, o, kPix * C, true);
+        } else {
+            for (int q = q0; q < npx; ++q)
+                for (int c = 0; c < C; ++c) tile[q * C + c] = Out<OUT>::cvt(Elem<TI>::f(s[c * HW + q]));
+        }
+        __syncthreads();
+        const int64_t nbytes = npx * C * (int64_t)sizeof(TO);
+        uint4* d16 = reinterpret_cast<uint4*>(dst + (r * HW + p0) * C);
+        const uint4* s16 = reinterpret_cast<const uint4*>(tile);
+        for (int64_t j = threadIdx.x; j < nbytes / 16; j += kStageThreads) d16[j] = s16[j];
+        for (int64_t b = (nbytes / 16) * 16 + threadIdx.x; b < nbytes; b += kStageThreads)
+            reinterpret_cast<unsigned char*>(d16)[b] = smem_raw[b];
+        __syncthreads();
+    }
+}
+
+static int stage_path() {
+    static int path = -1;
+    if (path < 0) {
+        const char* e = getenv("MBS_K2_PATH");   // A/B only: 0 = per-row, 1 = grid-stride vec, 2 = smem (default)
+        path = e ? atoi(e) : 2;
+    }
+    return path;
+}
+
 static int resident_grid(int64_t units) {
     static int sms = 0;
     if (!sms) {
@@ -276,7 +330,28 @@ static int stage_typed(const void* src, const int64_t* rows, int64_t row0, int64
         const bool nhwc = layout == MBS_NHWC && C > 1;
         const bool plane_ok = (HW % kPix == 0) && ((HW * (int64_t)sizeof(TI)) % 16 == 0) && (sa % 16 == 0) &&
                               (da % 16 == 0) && ((kPix * sizeof(TO)) % 16 == 0);
-        if (plane_ok && (layout == MBS_NCHW || layout == MBS_NHWC) && C >= 1 && C <= 4) {
+        const int path = stage_path();
+        if (path == 2 && nhwc && C <= 4 && (HW * (int64_t)sizeof(TI)) % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
+            ((int64_t)kTilePx * C * sizeof(TO)) % 16 == 0 && (HW * C * (int64_t)sizeof(TO)) % 16 == 0) {
+            const int64_t tpr = (HW + kTilePx - 1) / kTilePx, total = n_rows * tpr;
+            const size_t sm = (size_t)kTilePx * C * sizeof(TO);
+            const int grid = (int)std::min<int64_t>(total, resident_grid(total * kStageThreads));
+#define MBS_STAGE_SMEM(CC)                                                                                   \
+    do {                                                                                                     \
+        auto kern = k_stage_nhwc_smem<TI, OUT, CC>;                                                          \
+        if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+        kern<<<grid, kStageThreads, sm, st>>>(s, rows, row0, HW, tpr, total, d);                             \
+    } while (0)
+            switch (C) {
+                case 2: MBS_STAGE_SMEM(2); break;
+                case 3: MBS_STAGE_SMEM(3); break;
+                default: MBS_STAGE_SMEM(4); break;
+            }
+#undef MBS_STAGE_SMEM
+            MBS_CK_LAUNCH("k_stage_nhwc_smem");
+            return MBS_OK;
+        }
+        if (path == 1 && plane_ok && (layout == MBS_NCHW || layout == MBS_NHWC) && C >= 1 && C <= 4) {
             const int64_t upr = HW / kPix, total = n_rows * upr;
             const int grid = resident_grid((total + 1) / 2);
 #define MBS_STAGE_VEC(CC)                                                                                   \

@@ -94,7 +94,18 @@ def test_bucketed_equals_single_call(cuda):
     assert a1.micro_batches_seen == a2.micro_batches_seen == 2
     assert torch.equal(a1.flat, a2.flat)
     s1, s2 = a1.finalize(8), a2.finalize(8)
-    assert float(s1[0]) == float(s2[0])
+    # fused per-tile partials vs the post-hoc norm pass: same value, different summation grouping
+    assert float(s1[0]) == pytest.approx(float(s2[0]), rel=1e-12)
+    # run to run the same path is bit-reproducible (fixed-order reduction, no atomics)
+    a3 = mbs.GradientAccumulator(params)
+    a3.begin(2)
+    a3.add_tensors(grads, 0.25)
+    a3.add_tensors(grads, 0.25, last=True)
+    a4 = mbs.GradientAccumulator(params)
+    a4.begin(2)
+    a4.add_tensors(grads, 0.25)
+    a4.add_tensors(grads, 0.25, last=True)
+    assert float(a3.finalize(8)[0]) == float(a4.finalize(8)[0])
 
 
 def test_overflow_and_key_errors(cuda):
