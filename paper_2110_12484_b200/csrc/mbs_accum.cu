@@ -41,7 +41,7 @@ constexpr int kMaxPtrs = 1024;     // gradient pointers per K1 launch (kernel-pa
 #define MBS_K1_UNROLL 4
 #endif
 #ifndef MBS_K1_MINBLOCKS
-#define MBS_K1_MINBLOCKS 1
+#define MBS_K1_MINBLOCKS 4
 #endif
 constexpr int kUnroll = MBS_K1_UNROLL;
 
@@ -91,20 +91,21 @@ __device__ __forceinline__ int find_seg(const Seg* __restrict__ segs, int s0, in
     return a;
 }
 
-// One contiguous piece of one segment: acc[0..n) (+)= s * g[0..n).
+// One contiguous piece of one segment: acc[0..n) (+)= s * g[0..n). Pieces never exceed one CTA
+// share (<= 2^31 elements), so the inner loops use 32-bit indices (keeps K1 at ~56 registers).
 template <bool ASSIGN, bool NORM>
-__device__ __forceinline__ void accum_piece(float* __restrict__ a, const float* __restrict__ g, int64_t n, float s,
+__device__ __forceinline__ void accum_piece(float* __restrict__ a, const float* __restrict__ g, int n, float s,
                                             double& sq) {
-    int64_t done = 0;
+    int done = 0;
     if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
-        const int64_t n4 = n >> 2;
+        const int n4 = n >> 2;
         const float4* g4 = reinterpret_cast<const float4*>(g);
         float4* a4 = reinterpret_cast<float4*>(a);
-        for (int64_t base = threadIdx.x; base < n4; base += kThreads * kUnroll) {
+        for (int base = threadIdx.x; base < n4; base += kThreads * kUnroll) {
             float4 gv[kUnroll], av[kUnroll];
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
-                const int64_t i = base + u * kThreads;
+                const int i = base + u * kThreads;
                 if (i < n4) {
                     gv[u] = ld_stream(g4 + i);
                     if (!ASSIGN) av[u] = a4[i];
@@ -112,7 +113,7 @@ __device__ __forceinline__ void accum_piece(float* __restrict__ a, const float* 
             }
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
-                const int64_t i = base + u * kThreads;
+                const int i = base + u * kThreads;
                 if (i < n4) {
                     float4 r;
                     if (ASSIGN) {
@@ -128,7 +129,7 @@ __device__ __forceinline__ void accum_piece(float* __restrict__ a, const float* 
         }
         done = n4 << 2;
     }
-    for (int64_t i = done + threadIdx.x; i < n; i += kThreads) {  // tail / unaligned gradient
+    for (int i = done + threadIdx.x; i < n; i += kThreads) {  // tail / unaligned gradient
         const float r = ASSIGN ? s * g[i] : fmaf(s, g[i], a[i]);
         a[i] = r;
         if (NORM) sq += (double)r * (double)r;
@@ -140,8 +141,9 @@ __device__ __forceinline__ void accum_piece(float* __restrict__ a, const float* 
 // acc = s*g (ASSIGN) or acc += s*g; NORM adds this CTA's sum of squares to partials[b].
 template <bool ASSIGN, bool NORM>
 __global__ void __launch_bounds__(kThreads, MBS_K1_MINBLOCKS)
-k_accum(float* __restrict__ acc, const Seg* __restrict__ segs, int seg0, int seg1, int64_t lo0, int64_t hi0,
-        int64_t per_block, const __grid_constant__ GradPtrs gp, float s, double* __restrict__ partials,
+k_accum(float* __restrict__ acc, const Seg* __restrict__ segs, const int* __restrict__ tile_seg, int seg0, int seg1,
+        int64_t lo0, int64_t hi0, int64_t per_block, const __grid_constant__ GradPtrs gp, float s,
+        double* __restrict__ partials,
         const float* __restrict__ loss, double* __restrict__ loss_slot, double* __restrict__ factor_slot,
         double factor, double* __restrict__ weight_slot, double weight) {
     __shared__ double red[kThreads / 32];
@@ -149,11 +151,14 @@ k_accum(float* __restrict__ acc, const Seg* __restrict__ segs, int seg0, int seg
     const int64_t hi = min(lo + per_block, hi0);
     double sq = 0.0;
     if (lo < hi) {
-        for (int si = find_seg(segs, seg0, seg1, lo); si < seg1; ++si) {
+        // full-range launches read their first segment from a precomputed table (one load instead of a
+        // chain of dependent binary-search loads at every CTA start)
+        const int first = tile_seg != nullptr ? tile_seg[blockIdx.x] : find_seg(segs, seg0, seg1, lo);
+        for (int si = first; si < seg1; ++si) {
             const Seg sg = segs[si];
             if (sg.off >= hi) break;
             const int64_t p0 = max(lo, sg.off), p1 = min(hi, sg.off + sg.num);
-            if (p1 > p0) accum_piece<ASSIGN, NORM>(acc + p0, gp.p[si - seg0] + (p0 - sg.off), p1 - p0, s, sq);
+            if (p1 > p0) accum_piece<ASSIGN, NORM>(acc + p0, gp.p[si - seg0] + (p0 - sg.off), (int)(p1 - p0), s, sq);
         }
     }
     if (NORM) {
@@ -337,6 +342,7 @@ struct mbs_accum {
     double* d_partials = nullptr;      // [grid] ||acc||^2 partials, one per CTA of the last NORM launch
     int n_partials = 0;                // valid partials (0 = stale: finalize recomputes the norm)
     int64_t tile = kDefaultTile;       // elements per CTA (0 = balanced over resident CTAs)
+    int* d_tile_seg = nullptr;         // first segment of every full-range tile (tile > 0)
     int64_t max_partials = 0;
     double* d_losses = nullptr;        // [max_micro] raw loss per local micro-batch
     double* d_factors = nullptr;       // [max_micro]
@@ -435,7 +441,20 @@ int mbs_accum_create(float* acc_dev, int64_t acc_numel, int64_t n_segments,
     if (const char* t = getenv("MBS_K1_TILE")) h->tile = atoll(t);
     if (h->tile > 0 && h->tile < 1024) h->tile = 1024;
     h->max_partials = std::max<int64_t>(h->grid, (acc_numel + 1023) / 1024);
+    std::vector<int> tile_seg;
+    if (h->tile > 0) {
+        const int64_t lo = h->off[0], hi = h->off.back() + h->num.back();
+        const int64_t per = (h->tile + 31) / 32 * 32;
+        size_t si = 0;
+        for (int64_t t = lo; t < hi; t += per) {
+            while (si + 1 < segs.size() && segs[si + 1].off <= t) ++si;   // last segment with off <= t
+            tile_seg.push_back((int)si);
+        }
+    }
     cudaError_t e = cudaMalloc(&h->d_segs, sizeof(Seg) * segs.size());
+    if (e == cudaSuccess && !tile_seg.empty()) e = cudaMalloc(&h->d_tile_seg, sizeof(int) * tile_seg.size());
+    if (e == cudaSuccess && !tile_seg.empty())
+        e = cudaMemcpy(h->d_tile_seg, tile_seg.data(), sizeof(int) * tile_seg.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(h->d_segs, segs.data(), sizeof(Seg) * segs.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&h->d_partials, sizeof(double) * h->max_partials);
     if (e == cudaSuccess) e = cudaMemset(h->d_partials, 0, sizeof(double) * h->max_partials);
@@ -454,6 +473,7 @@ int mbs_accum_create(float* acc_dev, int64_t acc_numel, int64_t n_segments,
 int mbs_accum_destroy(mbs_accum_t h) {
     if (!h) return MBS_OK;
     if (h->d_segs) cudaFree(h->d_segs);
+    if (h->d_tile_seg) cudaFree(h->d_tile_seg);
     if (h->d_partials) cudaFree(h->d_partials);
     if (h->d_losses) cudaFree(h->d_losses);
     delete h;
@@ -511,17 +531,18 @@ static int launch_accum(mbs_accum_t h, const float* const* grads, int64_t seg_be
         const int64_t per = share(hi - lo, h->grid, h->tile);
         const unsigned grid = (unsigned)((hi - lo + per - 1) / per);
         const float* lp = (b == 0) ? loss_dev : nullptr;
+        const int* ts = (h->d_tile_seg != nullptr && s0 == 0 && s1 == (int)nseg) ? h->d_tile_seg : nullptr;
         double* ls = h->d_losses + slot;
         double* fs = h->d_factors + slot;
         double* ws = h->d_weights + slot;
         if (assign && norm)
-            k_accum<true, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
+            k_accum<true, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, ts, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
         else if (assign)
-            k_accum<true, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
+            k_accum<true, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, ts, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
         else if (norm)
-            k_accum<false, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
+            k_accum<false, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, ts, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
         else
-            k_accum<false, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
+            k_accum<false, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, ts, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
         MBS_CK_LAUNCH("k_accum");
         h->n_partials = norm ? (int)grid : 0;
     }
