@@ -193,6 +193,33 @@ int mbs_streamer_timing(mbs_streamer_t h, int64_t job, double* gather_ms, double
 int mbs_host_gather(const void* src, int64_t row_bytes, const int64_t* rows, int64_t n_rows,
                     void* dst, int n_threads);
 
+/* ---------------------------------------------------------------------------
+ * Fused last-micro-batch accumulate + all-reduce over peer memory (K1C) — the
+ * data-parallel exchange of SURVEY §8e (no reference equivalent) as ONE
+ * kernel: X_self = acc (+)= factor*g, reduce-scatter over the peers' X in rank
+ * order, all-gather into acc. Exchange buffers are exported with CUDA IPC
+ * (NVLink/NVSwitch P2P between the GPUs of a node).
+ * ------------------------------------------------------------------------- */
+#define MBS_PEER_HANDLE_BYTES 128
+typedef struct mbs_peer* mbs_peer_t;
+
+/* Allocate this rank's exchange buffer (numel floats, numel % 4 == 0) and signal block. */
+int mbs_peer_create(int rank, int world, int64_t numel, mbs_peer_t* out);
+/* Export this rank's IPC handles (MBS_PEER_HANDLE_BYTES bytes) for the other ranks. */
+int mbs_peer_handle(mbs_peer_t h, void* out);
+/* Map every peer's exchange buffer: `handles` holds world x MBS_PEER_HANDLE_BYTES bytes, rank order. */
+int mbs_peer_open(mbs_peer_t h, const void* handles);
+int mbs_peer_destroy(mbs_peer_t h);
+/* Device error flag (1 = a peer did not arrive within the timeout); synchronous. */
+int mbs_peer_status(mbs_peer_t h, int* error_flag);
+/* The last micro-batch of this rank: acc := SUM_ranks(acc_r (+)= factor*g_r) on every rank, as
+ * mbs_accum_add would (loss record, overflow guard) followed by an all-reduce. `grads` may be NULL
+ * for a rank without a micro-batch in this mini-batch (it contributes its accumulator). Spin-waits
+ * are bounded by timeout_ms; on timeout the device error flag is set and the kernel drains. */
+int mbs_accum_add_allreduce(mbs_accum_t h, mbs_peer_t peer, const float* const* grads, double factor,
+                            const float* loss_dev, double loss_factor, double loss_weight,
+                            double timeout_ms, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,6 +22,7 @@ NORM_MODES = {"paper_faithful": 0, "exact_weighted": 1, "off": 2}
 U8, F32, BF16, F16, F64 = range(5)
 NCHW, NHWC = 0, 1
 MAX_PARTS = 4
+PEER_HANDLE_BYTES = 128
 
 
 class Part(ctypes.Structure):
@@ -65,6 +66,13 @@ _SIGS = {
     "mbs_streamer_timing": (c_int, [c_void_p, c_int64, POINTER(c_double), POINTER(c_double), POINTER(c_double),
                                     POINTER(c_int64)]),
     "mbs_host_gather": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int]),
+    "mbs_peer_create": (c_int, [c_int, c_int, c_int64, POINTER(c_void_p)]),
+    "mbs_peer_handle": (c_int, [c_void_p, c_void_p]),
+    "mbs_peer_open": (c_int, [c_void_p, c_void_p]),
+    "mbs_peer_destroy": (c_int, [c_void_p]),
+    "mbs_peer_status": (c_int, [c_void_p, POINTER(c_int)]),
+    "mbs_accum_add_allreduce": (c_int, [c_void_p, c_void_p, POINTER(c_void_p), c_double, c_void_p, c_double,
+                                        c_double, c_double, c_void_p]),
 }
 
 EXPORTS = tuple(_SIGS)

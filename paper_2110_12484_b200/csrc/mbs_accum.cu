@@ -354,6 +354,26 @@ struct mbs_accum {
     int64_t covered = 0;               // segments added so far for the current micro-batch
 };
 
+namespace mbs {
+int accum_view(mbs_accum_t h, AccumView* v) {
+    if (!h || !v) return invalid("null accumulator");
+    v->acc = h->acc;
+    v->numel = h->numel;
+    v->off = &h->off;
+    v->num = &h->num;
+    v->d_losses = h->d_losses;
+    v->d_factors = h->d_factors;
+    v->d_weights = h->d_weights;
+    v->seen = &h->seen;
+    v->covered = &h->covered;
+    v->expected = h->expected;
+    v->max_micro = h->max_micro;
+    v->fresh = &h->fresh;
+    v->n_partials = &h->n_partials;
+    return MBS_OK;
+}
+}  // namespace mbs
+
 extern "C" {
 
 const char* mbs_status_string(int s) {

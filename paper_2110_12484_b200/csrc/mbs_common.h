@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <vector>
 
 #include "../../include/mbs.h"
 
@@ -20,6 +21,24 @@ inline int invalid(const std::string& msg) {
     set_error(msg);
     return MBS_EINVAL;
 }
+
+// Internal view of an accumulator handle (mbs_accum.cu) for the fused peer all-reduce (mbs_peer.cu).
+struct AccumView {
+    float* acc;
+    int64_t numel;
+    const std::vector<int64_t>* off;
+    const std::vector<int64_t>* num;
+    double* d_losses;
+    double* d_factors;
+    double* d_weights;
+    int64_t* seen;
+    int64_t* covered;
+    int64_t expected;
+    int64_t max_micro;
+    bool* fresh;
+    int* n_partials;
+};
+int accum_view(mbs_accum_t h, AccumView* v);
 
 }  // namespace mbs
 

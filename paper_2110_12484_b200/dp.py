@@ -12,8 +12,10 @@ rank (at most one micro-batch of imbalance). Each rank:
    the single-device one;
 2. on its LAST micro-batch, accumulates gradient BUCKETS as autograd produces
    them (post-accumulate-grad hooks) and immediately launches an async NCCL
-   SUM all-reduce of that bucket's slice of the flat accumulator, so the
-   all-reduce overlaps the rest of the backward (SURVEY.md §8e);
+   SUM all-reduce of that bucket's slice of the flat accumulator (in a fixed
+   bucket order), so the all-reduce overlaps the rest of the backward
+    — or, with ``transport="peer"``, runs the last K1 and the
+   all-reduce as ONE kernel over CUDA-IPC peer memory (K1C, ``mbs_peer.cu``);
 3. after the last bucket, recomputes the grad norm of the reduced sum (the
    optimizer's non-finite guard), all-reduces the tiny loss record, and runs
    the identical K3 step on every rank.
@@ -129,16 +131,64 @@ class _Result:
     outputs = None
 
 
-class DataParallelMBS:
-    """Per-rank driver of data-parallel micro-batch streaming (torch.distributed, NCCL)."""
+class PeerExchange:
+    """Symmetric exchange buffers for the fused K1 + all-reduce over peer memory (``mbs_peer_*``).
 
-    def __init__(self, params: ParameterSet, process_group=None, bucket_mb: float = 32.0):
+    Every rank allocates its buffer in the native library, exports CUDA IPC
+    handles, and maps every peer's buffer (NVLink/NVSwitch P2P inside a node;
+    ranks sharing one GPU also work, which is how it is tested on one B200).
+    """
+
+    def __init__(self, numel: int, group=None):
+        import ctypes
+
         import torch.distributed as dist
+        from . import _native as N
+        self.N = N
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        h = ctypes.c_void_p()
+        N.check(N.lib().mbs_peer_create(self.rank, self.world, int(numel), ctypes.byref(h)), "mbs_peer_create")
+        self.handle = h
+        mine = (ctypes.c_char * N.PEER_HANDLE_BYTES)()
+        N.check(N.lib().mbs_peer_handle(h, mine), "mbs_peer_handle")
+        allh = [None] * self.world
+        dist.all_gather_object(allh, bytes(mine), group=group)
+        buf = (ctypes.c_char * (N.PEER_HANDLE_BYTES * self.world)).from_buffer_copy(b"".join(allh))
+        N.check(N.lib().mbs_peer_open(h, buf), "mbs_peer_open")
+        dist.barrier(group=group)
+
+    def error(self) -> bool:
+        import ctypes
+        v = ctypes.c_int()
+        self.N.check(self.N.lib().mbs_peer_status(self.handle, ctypes.byref(v)), "mbs_peer_status")
+        return bool(v.value)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.N.lib().mbs_peer_destroy(self.handle)
+            self.handle = None
+
+
+class DataParallelMBS:
+    """Per-rank driver of data-parallel micro-batch streaming.
+
+    ``transport="nccl"`` (default): bucket-wise K1 from post-accumulate-grad hooks + async NCCL
+    all-reduce overlapped with the last backward. ``transport="peer"``: the last micro-batch's K1
+    and the all-reduce are ONE kernel over peer memory (``PeerExchange``, K1C).
+    """
+
+    def __init__(self, params: ParameterSet, process_group=None, bucket_mb: float = 32.0, transport: str = "nccl"):
+        import torch.distributed as dist
+        if transport not in ("nccl", "peer"):
+            raise ValueError(f"unknown transport {transport!r}")
         self.dist = dist
         self.params = params
         self.group = process_group
         self.world = dist.get_world_size(process_group)
         self.rank = dist.get_rank(process_group)
+        self.transport = transport
+        self.peer = PeerExchange(params.layout.total, process_group) if transport == "peer" else None
         self.buckets = bucket_ranges(params.layout.numels, max(1, int(bucket_mb * 2 ** 20 / 4)))
         self._seg_bucket = {}
         for b, (s0, s1) in enumerate(self.buckets):
@@ -188,9 +238,24 @@ class DataParallelMBS:
                 loss.backward()
                 acc.add_module_grads(f, loss=loss, loss_factor=f, loss_weight=plan.sizes[k])
                 continue
-            # last micro-batch: bucket-wise K1 + async all-reduce, overlapped with the rest of backward
+            if self.peer is not None:
+                loss.backward()
+                acc.add_allreduce(self.peer, f, loss=loss, loss_factor=f, loss_weight=plan.sizes[k])
+                continue
+            # last micro-batch: bucket-wise K1 + async all-reduce, overlapped with the rest of backward.
+            # All-reduces are issued strictly in self.buckets order (a bucket that completes early waits
+            # for its predecessors), so every rank — including one without a micro-batch — issues the
+            # identical collective sequence.
             pending = {b: s1 - s0 for b, (s0, s1) in enumerate(self.buckets)}
+            done = set()
+            nxt = [0]
             handles = []
+
+            def launch_ready():
+                while nxt[0] in done:
+                    s0, s1 = self.buckets[nxt[0]]
+                    works.append(self.dist.all_reduce(self._slice(acc, s0, s1), group=self.group, async_op=True))
+                    nxt[0] += 1
 
             def hook(p, _idx={id(q): i for i, q in enumerate(plist)}):
                 s = _idx[id(p)]
@@ -202,7 +267,8 @@ class DataParallelMBS:
                                     loss=loss if s0 == 0 else None, loss_factor=f, loss_weight=plan.sizes[k])
                     for i in range(s0, s1):
                         plist[i].grad = None
-                    works.append(self.dist.all_reduce(self._slice(acc, s0, s1), group=self.group, async_op=True))
+                    done.add(b)
+                    launch_ready()
 
             for p in plist:
                 handles.append(p.register_post_accumulate_grad_hook(hook))
@@ -214,12 +280,19 @@ class DataParallelMBS:
             if any(v != 0 for v in pending.values()):
                 from .errors import AccumulatorOverflowError
                 raise AccumulatorOverflowError("a parameter received no gradient on the last micro-batch")
+            launch_ready()
         if own is not None:
             own.close()
         for wk in works:
             wk.wait()
         if n_local == 0:
             acc.begin(0)
+            if self.peer is not None:     # no micro-batch here: still take part in the exchange
+                acc.add_allreduce(self.peer, 1.0, from_module=False)
+            else:                         # same bucket sequence as the working ranks, zeros contributed
+                acc._materialize()
+                for s0, s1 in self.buckets:
+                    self.dist.all_reduce(self._slice(acc, s0, s1), group=self.group)
         # grad norm of the REDUCED sum (the optimizer's guard) + the global loss record
         stats_dev = acc.finalize(plan.n_b, recompute_norm=True)
         rec = torch.zeros(1 + 2 * plan.n_s_mu, dtype=torch.float64, device=acc.flat.device)

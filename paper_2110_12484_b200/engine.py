@@ -293,6 +293,43 @@ class GradientAccumulator:
         for p in self._plist:
             p.grad = None
 
+    def add_allreduce(self, peer, factor: float, *, from_module: bool = True, tensors: list | None = None,
+                      loss: torch.Tensor | None = None, loss_factor: float | None = None, loss_weight: float = 0.0,
+                      timeout_ms: float = 60_000.0, stream=None) -> None:
+        """K1C: this rank's last micro-batch fused with the all-reduce over peer memory (``mbs_accum_add_allreduce``).
+
+        With ``from_module`` the gradients are the parameters' ``.grad`` tensors (then released);
+        ``from_module=False`` and ``tensors=None`` contributes only the accumulator (a rank without a
+        micro-batch in this mini-batch).
+        """
+        ptrs, keep = None, []
+        if from_module or tensors is not None:
+            src = [p.grad for p in self._plist] if from_module else list(tensors)
+            ptrs = self._ptr_table
+            for j, g in enumerate(src):
+                if g is None:
+                    raise AccumulatorOverflowError("gradient keys do not match accumulator parameters "
+                                                   "(a parameter received no gradient)")
+                g = self._conform(g, j)
+                keep.append(g)
+                ptrs[j] = g.data_ptr()
+        lp = None
+        if loss is not None:
+            loss = loss.detach().float()
+            keep.append(loss)
+            lp = loss.data_ptr()
+        lf = float(factor if loss_factor is None else loss_factor)
+        t0 = TIMER.start(stream)
+        N.check(N.lib().mbs_accum_add_allreduce(self._h, peer.handle, ptrs, float(factor), lp, lf, float(loss_weight),
+                                                float(timeout_ms), _stream_ptr(stream)), "mbs_accum_add_allreduce")
+        TIMER.stop("k1c_accumulate_allreduce", t0, 12 * self.layout.n_params, stream)
+        self._fresh = False
+        self._covered = 0
+        self._pending_zero = False
+        if from_module:
+            for p in self._plist:
+                p.grad = None
+
     def finalize(self, n_b: int, *, recompute_norm: bool = False, stream=None) -> torch.Tensor:
         """Reduce the grad-norm partials and the loss record into ``stats_dev`` (device)."""
         if recompute_norm:

@@ -64,7 +64,7 @@ def _rank(rank, world, port, backend, n_per_rank, n_mu, mode, q):
         dist.destroy_process_group()
 
 
-def _single(n_b, n_mu, mode):
+def _single(n_b, n_mu, mode, steps=2):
     import paper_2110_12484_b200 as mbs
     torch.backends.cudnn.allow_tf32 = False
     dev = torch.device("cuda:0")
@@ -74,7 +74,7 @@ def _single(n_b, n_mu, mode):
     st = mbs.sgd_state(0.05, 0.9, 5e-4)
     out = []
     acc = mbs.GradientAccumulator(params)
-    for step in range(2):
+    for step in range(steps):
         _, s = mbs.train_mini_batch(net, params, (x.to(dev), y.to(dev)), mbs.plan_split(n_b, n_mu), mode,
                                     "cross_entropy", st, accumulator=acc)
         out.append((s.loss, list(s.losses_raw), s.grad_norm, s.step_count))
@@ -116,3 +116,59 @@ def test_one_rank_nccl(cuda):
     w_single, out_single = _single(12, 4, "exact_weighted")
     err = np.linalg.norm(res[0][1] - w_single) / np.linalg.norm(w_single)
     assert err <= 1e-6, err
+
+
+def _rank_peer(rank, world, port, n_per_rank, n_mu, mode, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2110_12484_b200 as mbs
+        from paper_2110_12484_b200.dp import DataParallelMBS
+        dev = torch.device("cuda:0")
+        net = _net().to(dev)
+        params = mbs.ParameterSet(net)
+        x, y = _data(n_per_rank * world)
+        xs, ys = x[rank * n_per_rank:(rank + 1) * n_per_rank], y[rank * n_per_rank:(rank + 1) * n_per_rank]
+        d = DataParallelMBS(params, transport="peer")
+        st = mbs.sgd_state(0.05, 0.9, 5e-4)
+        acc = mbs.GradientAccumulator(params)
+        out = []
+        for step in range(3):
+            r = d.train_mini_batch(net, (xs.to(dev), ys.to(dev)), n_per_rank, n_mu, mode, "cross_entropy", st,
+                                   accumulator=acc)
+            out.append((r.loss, list(r.losses_raw), r.grad_norm, r.step_count))
+        torch.cuda.synchronize()
+        assert not d.peer.error()
+        q.put((rank, params.flat.cpu().numpy().copy(), out, acc.flat.cpu().numpy().copy()))
+        dist.barrier()
+        d.peer.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_peer_allreduce_two_ranks_one_gpu(cuda):
+    """K1C: last-micro accumulate + all-reduce in one kernel over CUDA-IPC peer memory (2 ranks, 1 GPU)."""
+    n_per_rank, n_mu, mode = 12, 4, "exact_weighted"
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_peer, args=(r, 2, port, n_per_rank, n_mu, mode, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    np.testing.assert_array_equal(res[0][1], res[1][1])       # identical weights on both ranks
+    np.testing.assert_array_equal(res[0][3], res[1][3])       # identical reduced accumulators
+    w_single, out_single = _single(2 * n_per_rank, n_mu, mode, steps=3)
+    err = np.linalg.norm(res[0][1] - w_single) / np.linalg.norm(w_single)
+    assert err <= 1e-6, err
+    for (l, raw, gn, sc), (l1, raw1, gn1, sc1) in zip(res[0][2], out_single):
+        assert sc == sc1
+        assert l == pytest.approx(l1, rel=1e-5)
+        np.testing.assert_allclose(raw, raw1, rtol=1e-5)
+        assert gn == pytest.approx(gn1, rel=1e-5)
