@@ -239,7 +239,7 @@ def main():
     dp = None
     if ws > 1:
         from paper_2110_12484_b200.dp import DataParallelMBS
-        dp = DataParallelMBS(params)
+        dp = DataParallelMBS(params, transport=os.environ.get("MBS_DP_TRANSPORT", "nccl"))
 
     def make_opt():
         return mbs.sgd_state(0.01, 0.9, 5e-4) if w.optimizer == "sgd" else mbs.adam_state(0.01, 5e-4)
