@@ -117,3 +117,21 @@ def measure_budget(model: torch.nn.Module, make_batch, loss_kind: str, *, optimi
     resident = max(held, parameter_space_bytes(n_params, optimizer_kind))
     return MemoryBudget(capacity_bytes=capacity, param_bytes=resident, data_bytes_per_sample=int(per_sample),
                         fixed_overhead_bytes=int(overhead))
+
+
+def bn_safe_micro_batch(n_b: int, n_mu: int) -> int:
+    """Largest micro-batch size <= n_mu whose plan (engine.py:56-78) has no 1-sample micro-batch.
+
+    The reference allows a 1-sample tail (e.g. 33/16 -> [16, 16, 1]); torch's
+    BatchNorm cannot train on one sample when a channel then holds a single
+    value (BatchNorm1d, or 1x1 spatial maps). The auto-sizer applies this guard
+    to BN models; the plan itself is never altered.
+    """
+    if n_b < 1 or n_mu < 1:
+        raise ValueError("batch sizes must be positive")
+    if n_b == 1:
+        return 1
+    m = min(n_mu, n_b)
+    while m > 1 and n_b % m == 1:
+        m -= 1
+    return m

@@ -284,7 +284,48 @@ def main():
     np.savez_compressed(os.path.join(HERE, "epoch.npz"), **arrays)
     with open(os.path.join(HERE, "misc.json"), "w") as f:
         json.dump(gen_misc(), f)
+    meta, arrays = gen_losses_metrics()
+    with open(os.path.join(HERE, "losses.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+    np.savez_compressed(os.path.join(HERE, "losses.npz"), **arrays)
     print("golden fixtures written to", HERE)
+
+
+def gen_losses_metrics():
+    """Reference losses (value) and metrics on small random inputs (losses.py:72-263)."""
+    from mbstream import losses
+    rs = np.random.RandomState(8)
+    out, arrays = {"losses": [], "metrics": []}, {}
+    for i in range(6):
+        n = int(rs.randint(1, 6))
+        logits = rs.randn(n, 5) * 3
+        cls = rs.randint(0, 5, size=n)
+        z = rs.randn(n, 1, 4, 4) * 2
+        t = (rs.rand(n, 1, 4, 4) < 0.5).astype(np.float64)
+        d = rs.randn(n, 3)
+        td = rs.randn(n, 3)
+        p = 1.0 / (1.0 + np.exp(-z))
+        for nm, v in (("logits", logits), ("cls", cls), ("z", z), ("t", t), ("d", d), ("td", td)):
+            arrays[f"l{i}/{nm}"] = v
+        rec = {"i": i,
+               "mse": losses.compute_loss("mse", d, td).value.hex(),
+               "cross_entropy": losses.compute_loss("cross_entropy", logits, cls).value.hex(),
+               "bce_logits": losses.compute_loss("bce", z, t, from_logits=True).value.hex(),
+               "bce_probs": losses.compute_loss("bce", p, t, from_logits=False).value.hex(),
+               "bce_dice_logits": losses.compute_loss("bce_dice", z, t, from_logits=True).value.hex(),
+               "bce_dice_probs": losses.compute_loss("bce_dice", p, t, from_logits=False).value.hex(),
+               "accuracy": losses.accuracy(logits, cls)}
+        pair = losses.MaskPair(p, t)
+        for thr in (0.3, 0.5):
+            for per in (False, True):
+                rec[f"dice_{thr}_{per}"] = losses.dice_coefficient(pair, thr, per)
+                rec[f"iou_{thr}_{per}"] = losses.iou(pair, thr, per)
+        out["losses"].append(rec)
+    # empty masks -> 1.0 (losses.py:224-233)
+    z0 = np.zeros((2, 1, 3, 3))
+    pair0 = losses.MaskPair(z0, z0)
+    out["empty"] = [losses.dice_coefficient(pair0), losses.iou(pair0, per_image=True)]
+    return out, arrays
 
 
 if __name__ == "__main__":

@@ -41,3 +41,16 @@ def test_overhead_report():
     assert streaming.overhead_report(a, None).baseline_failed
     m = streaming.measured_schedule([1.0, 1.0, 1.0], [30.0, 30.0, 30.0], 0.5)
     assert m.makespan == pytest.approx((1.0 + 90.0 + 0.5) / 1e3)
+
+
+def test_bn_safe_micro_batch():
+    from paper_2110_12484_b200.memory import bn_safe_micro_batch
+    assert bn_safe_micro_batch(33, 16) == 15            # 33/16 -> [16,16,1]; 33/15 -> [15,15,3]
+    assert bn_safe_micro_batch(64, 8) == 8
+    assert bn_safe_micro_batch(2, 5) == 2
+    assert bn_safe_micro_batch(1, 5) == 1
+    for n_b in range(2, 200):
+        for n_mu in (1, 2, 3, 7, 16, 48, 128):
+            m = bn_safe_micro_batch(n_b, n_mu)
+            assert 1 <= m <= n_mu
+            assert min(mbs.plan_split(n_b, m).sizes) > 1 or m == 1
