@@ -226,13 +226,14 @@ def main():
         torch.cuda.empty_cache()
     plan = mbs.plan_split(n_b, n_mu)
 
-    # N=1: the timed region is ONE call of the public epoch API (engine.train_epoch, engine.py:276)
-    # over `steps` mini-batches in the reference's shuffled order (device rows gathered by K2, host rows
-    # by the native gather pool + H2D). N>1: per-step DataParallelMBS over two alternating mini-batches.
-    # Either way every mini-batch is >= 154 MB of uint8, so inputs exceed the 126 MB L2.
-    epoch_mode = ws == 1
+    # The timed region is ONE epoch call over `steps` shuffled mini-batches: engine.train_epoch
+    # (engine.py:276) at N=1, DataParallelMBS.train_epoch (each rank streams its own shard, one
+    # all-reduce per global mini-batch) at N>1. Device rows are gathered by K2, host rows by the native
+    # gather pool + H2D. Every mini-batch is >= 154 MB of uint8, so inputs exceed the 126 MB L2.
     warm_mini = min(n_b, 1024)           # warm-up mini-batches (C4's 300k-sample mini-batch is 66 s of compute)
-    n_data = max(args.steps * n_b, args.warmup * warm_mini) if epoch_mode else 2 * n_b
+    if ws > 1:
+        warm_mini = n_b                  # the global plan needs every rank's local mini-batch to be whole micros
+    n_data = max(args.steps * n_b, args.warmup * warm_mini)
     x_host, y_host = synthetic_data(w, n_data, seed=rank, pinned=True)
     x_dev, y_dev = x_host.to(dev), y_host.to(dev)
 
@@ -249,15 +250,15 @@ def main():
     streamer = mbs.make_streamer(x_host, y_host, n_mu, n_slots=3)
     cs = torch.cuda.current_stream(dev)
 
-    def step(i, host: bool):
-        sl = slice((i % 2) * n_b, (i % 2 + 1) * n_b)
-        x, y = (x_host[sl], y_host[sl]) if host else (x_dev[sl], y_dev[sl])
-        return dp.train_mini_batch(model, (x, y), n_b, n_mu, w.normalization, w.loss_kind, st, accumulator=acc,
-                                   staging=staging, autocast_dtype=autocast, streamer=streamer if host else None,
-                                   prefetch=True)
-
     def epoch(host: bool, n_steps: int, epoch_index: int, mini: int = n_b):
         xs, ys = (x_host, y_host) if host else (x_dev, y_dev)
+        if dp is not None:
+            res = dp.train_epoch(model, xs[:n_steps * mini], ys[:n_steps * mini], mini_batch_size=mini,
+                                 micro_batch_size=n_mu, normalization=w.normalization, loss_kind=w.loss_kind,
+                                 optimizer_state=st, seed=rank, epoch_index=epoch_index, accumulator=acc,
+                                 staging=staging, autocast_dtype=autocast, streamer=streamer if host else None,
+                                 prefetch=True)
+            return [r.loss for r in res]
         es = mbs.train_epoch(model, params, xs[:n_steps * mini], ys[:n_steps * mini], mini_batch_size=mini,
                              micro_batch_size=n_mu, normalization=w.normalization, loss_kind=w.loss_kind,
                              optimizer_state=st, seed=rank, epoch_index=epoch_index, shuffle=True, prefetch=True,
@@ -271,11 +272,7 @@ def main():
         torch.cuda.synchronize(dev)
 
     def timed(host: bool, steps: int, warmup: int, k1_timer: bool):
-        if epoch_mode:
-            epoch(host, warmup, 1000 + int(host), warm_mini)
-        else:
-            for i in range(warmup):
-                step(i, host).resolve()
+        epoch(host, warmup, 1000 + int(host), warm_mini)
         barrier()
         TIMER.reset()
         TIMER.enabled = k1_timer
@@ -283,16 +280,7 @@ def main():
             streamer.timings(flush=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(cs)
-        if epoch_mode:
-            losses = epoch(host, steps, int(host))
-        else:
-            prev, losses = None, []
-            for i in range(steps):
-                s = step(i, host)
-                if prev is not None:
-                    losses.append(prev.loss)        # D2H read of the previous step's loss (one step behind)
-                prev = s
-            losses.append(prev.loss)
+        losses = epoch(host, steps, int(host))
         e1.record(cs)
         barrier()
         TIMER.enabled = False
@@ -371,10 +359,10 @@ def main():
                        "model_precision": "bf16 autocast on cuDNN/cuBLAS, fp32 master weights; MBS path fp32",
                        "input": "uint8 NCHW staged to bf16 NHWC by K2",
                        "l2": ("inputs > L2: every mini-batch is %.0f MB of uint8" % (x_dev[:n_b].numel() / 1e6)) +
-                             (", none reused within the timed region" if epoch_mode else
-                              ", two alternating per rank"),
-                       "api": "engine.train_epoch over `steps` shuffled mini-batches" if epoch_mode else
-                              "dp.DataParallelMBS.train_mini_batch per step",
+                             ", none reused within the timed region",
+                       "api": ("engine.train_epoch" if ws == 1 else "dp.DataParallelMBS.train_epoch (per-rank "
+                               "shards, one NCCL all-reduce per global mini-batch)") +
+                              " over `steps` shuffled mini-batches",
                        "autosize": autosize},
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": int(h2d_bytes),
                     "d2h_bytes_per_step": 8 * (4 + 2 * plan.n_s_mu), "ms_per_step": ms_host / args.steps},

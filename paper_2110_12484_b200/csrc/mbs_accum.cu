@@ -238,31 +238,35 @@ __device__ __forceinline__ void sgd4(float4& ww, float4& vv, const float4 gg, fl
     ww.z = fmaf(-lr, vv.z, ww.z); ww.w = fmaf(-lr, vv.w, ww.w);
 }
 
+#ifndef MBS_K3_UNROLL
+#define MBS_K3_UNROLL 2
+#endif
 template <bool READ_V, bool WD>
 __global__ void __launch_bounds__(kThreads)
 k_sgd(float4* __restrict__ w, const float4* __restrict__ g, float4* __restrict__ v, int64_t n4,
       float lr, float mu, float wd, const double* __restrict__ guard) {
     if (guard_tripped(guard)) return;
+    constexpr int U = MBS_K3_UNROLL;
     const int64_t stride = (int64_t)gridDim.x * kThreads;
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n4; i += 2 * stride) {
-        const int64_t i2 = i + stride;
-        const bool two = i2 < n4;
-        const float4 g0 = ld_stream(g + i);
-        float4 w0 = w[i];
-        float4 v0 = READ_V ? v[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 g1, w1, v1;
-        if (two) {
-            g1 = ld_stream(g + i2);
-            w1 = w[i2];
-            v1 = READ_V ? v[i2] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n4; i += U * stride) {
+        float4 gg[U], ww[U], vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t j = i + u * stride;
+            if (j < n4) {
+                gg[u] = ld_stream(g + j);
+                ww[u] = w[j];
+                vv[u] = READ_V ? v[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
-        sgd4<READ_V, WD>(w0, v0, g0, lr, mu, wd);
-        v[i] = v0;
-        w[i] = w0;
-        if (two) {
-            sgd4<READ_V, WD>(w1, v1, g1, lr, mu, wd);
-            v[i2] = v1;
-            w[i2] = w1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t j = i + u * stride;
+            if (j < n4) {
+                sgd4<READ_V, WD>(ww[u], vv[u], gg[u], lr, mu, wd);
+                v[j] = vv[u];
+                w[j] = ww[u];
+            }
         }
     }
 }

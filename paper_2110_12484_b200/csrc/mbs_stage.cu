@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -335,7 +336,9 @@ static int stage_typed(const void* src, const int64_t* rows, int64_t row0, int64
             ((int64_t)kTilePx * C * sizeof(TO)) % 16 == 0 && (HW * C * (int64_t)sizeof(TO)) % 16 == 0) {
             const int64_t tpr = (HW + kTilePx - 1) / kTilePx, total = n_rows * tpr;
             const size_t sm = (size_t)kTilePx * C * sizeof(TO);
-            const int grid = (int)std::min<int64_t>(total, resident_grid(total * kStageThreads));
+            // one CTA per tile (the block scheduler balances); MBS_K2_GRID=resident caps it at the resident CTAs
+            static const bool cap = getenv("MBS_K2_GRID") && strcmp(getenv("MBS_K2_GRID"), "resident") == 0;
+            const int grid = (int)std::min<int64_t>(total, cap ? resident_grid(total * kStageThreads) : 2147483647);
 #define MBS_STAGE_SMEM(CC)                                                                                   \
     do {                                                                                                     \
         auto kern = k_stage_nhwc_smem<TI, OUT, CC>;                                                          \

@@ -203,7 +203,8 @@ class DataParallelMBS:
 
     def train_mini_batch(self, model, batch, n_b_per_rank: int, n_mu: int, normalization: str, loss_kind: str,
                          optimizer_state, *, accumulator: GradientAccumulator, staging=None, autocast_dtype=None,
-                         streamer=None, prefetch=True, loss_from_logits=True, dice_smoothing=1.0):
+                         streamer=None, prefetch=True, loss_from_logits=True, dice_smoothing=1.0,
+                         lr_for_step=None):
         """Weak-scaling step: this rank's batch holds its own n_b_per_rank samples (= its block of the global plan)."""
         plan = weak_scaling_plan(n_b_per_rank, n_mu, self.world)
         block = partition_micro_batches(plan, self.world)[self.rank]
@@ -211,20 +212,87 @@ class DataParallelMBS:
         x, y = (_as_tensor(t) for t in batch)
         if x.shape[0] != hi - lo:
             raise ValueError(f"rank {self.rank} holds {x.shape[0]} samples, its block of the plan needs {hi - lo}")
-        acc = accumulator
-        n_local = block[1] - block[0]
-        acc.begin(n_local)
         jobs = [(None, plan.index_ranges[k][0] - lo, plan.sizes[k]) for k in range(*block)]
         own = None
         if x.device.type == "cpu" and streamer is None:
             streamer = own = make_streamer(x, y, n_mu)
-        source = _micro_source(x, y, jobs, staging, prefetch, streamer)
+        try:
+            source = iter(_micro_source(x, y, jobs, staging, prefetch, streamer))
+            return self._step(model, plan, block, source, normalization, loss_kind, optimizer_state, accumulator,
+                              autocast_dtype, loss_from_logits, dice_smoothing, lr_for_step)
+        finally:
+            if own is not None:
+                own.close()
+
+    def train_epoch(self, model, x, y, *, mini_batch_size: int, micro_batch_size: int, normalization: str,
+                    loss_kind: str, optimizer_state, seed: int, epoch_index: int, accumulator: GradientAccumulator,
+                    shuffle: bool = True, staging=None, autocast_dtype=None, streamer=None, prefetch=True,
+                    loss_from_logits=True, dice_smoothing=1.0, lr_for_step=None) -> list:
+        """One weak-scaling epoch: every rank walks ITS shard (x, y) in its own shuffled order.
+
+        Rank r's order is the reference's named stream extended by the rank,
+        ``named_stream(seed, f"shuffle/epoch{e}/rank{r}")`` (rng.py:26-28); global
+        mini-batch m is the union of every rank's m-th local mini-batch of
+        ``mini_batch_size`` samples, split by the global plan. All of the
+        rank's micro-batches of the epoch stream as one sequence (cross-step
+        prefetch). Returns the per-mini-batch statistics (resolved).
+        """
+        from .rng import named_stream
+        x, y = _as_tensor(x), _as_tensor(y)
+        n = x.shape[0]
+        if n == 0:
+            raise ValueError("dataset is empty")
+        if n % mini_batch_size:
+            raise ValueError("weak-scaling epochs need whole local mini-batches on every rank")
+        on_device = x.device.type == "cuda"
+        order = (named_stream(seed, f"shuffle/epoch{epoch_index}/rank{self.rank}").permutation(n) if shuffle
+                 else np.arange(n))
+        order_dev = torch.from_numpy(order.astype(np.int64)).to(x.device) if (on_device and shuffle) else None
+        plan = weak_scaling_plan(mini_batch_size, micro_batch_size, self.world)
+        block = partition_micro_batches(plan, self.world)[self.rank]
+        lo, _ = rank_samples(plan, block)
+        jobs = []
+        for start in range(0, n, mini_batch_size):
+            for k in range(*block):
+                a, b = plan.index_ranges[k]
+                a, b = start + a - lo, start + b - lo
+                if not shuffle:
+                    jobs.append((None, a, b - a))
+                elif on_device:
+                    jobs.append((order_dev[a:b], 0, b - a))
+                else:
+                    jobs.append((order[a:b], 0, b - a))
+        own = None
+        if not on_device and streamer is None:
+            streamer = own = make_streamer(x, y, micro_batch_size)
+        out = []
+        try:
+            source = iter(_micro_source(x, y, jobs, staging, prefetch, streamer))
+            for _ in range(0, n, mini_batch_size):
+                r = self._step(model, plan, block, source, normalization, loss_kind, optimizer_state, accumulator,
+                               autocast_dtype, loss_from_logits, dice_smoothing, lr_for_step)
+                if out:
+                    out[-1].resolve()          # one mini-batch behind: no stall
+                out.append(r)
+            for r in out:
+                r.resolve()
+        finally:
+            if own is not None:
+                own.close()
+        return out
+
+    def _step(self, model, plan, block, source, normalization, loss_kind, optimizer_state, acc, autocast_dtype,
+              loss_from_logits, dice_smoothing, lr_for_step):
+        """Consume this rank's micro-batches of one global mini-batch from `source`, exchange, step."""
+        n_local = block[1] - block[0]
+        acc.begin(n_local)
         ctx = torch.autocast("cuda", dtype=autocast_dtype) if autocast_dtype is not None else nullcontext()
         model.train()
         losses, factors, weights = [], [], []
         works = []
         plist = acc._plist
-        for j, (xk, yk) in enumerate(source):
+        for j in range(n_local):
+            xk, yk = next(source)
             k = block[0] + j
             f = normalization_factor(plan, k, normalization)
             last = j == n_local - 1
@@ -281,8 +349,6 @@ class DataParallelMBS:
                 from .errors import AccumulatorOverflowError
                 raise AccumulatorOverflowError("a parameter received no gradient on the last micro-batch")
             launch_ready()
-        if own is not None:
-            own.close()
         for wk in works:
             wk.wait()
         if n_local == 0:
@@ -306,6 +372,8 @@ class DataParallelMBS:
             rec[1 + plan.n_s_mu + k0:1 + plan.n_s_mu + k0 + n_local] = lv * fv
         self.dist.all_reduce(rec, group=self.group)
         total = acc.as_gradient_set()
+        if lr_for_step is not None:
+            optimizer_state.lr = lr_for_step(optimizer_state.step_count)
         apply_update(self.params, total, optimizer_state)
         res = _Result(rec, stats_dev[0], plan.n_s_mu)
         res.step_count = optimizer_state.step_count

@@ -172,3 +172,70 @@ def test_fused_peer_allreduce_two_ranks_one_gpu(cuda):
         assert l == pytest.approx(l1, rel=1e-5)
         np.testing.assert_allclose(raw, raw1, rtol=1e-5)
         assert gn == pytest.approx(gn1, rel=1e-5)
+
+
+def _rank_epoch(rank, world, port, shard, mini, n_mu, q, transport):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2110_12484_b200 as mbs
+        from paper_2110_12484_b200.dp import DataParallelMBS
+        dev = torch.device("cuda:0")
+        net = _net().to(dev)
+        params = mbs.ParameterSet(net)
+        x, y = _data(shard * world)
+        xs, ys = x[rank * shard:(rank + 1) * shard], y[rank * shard:(rank + 1) * shard]
+        d = DataParallelMBS(params, transport=transport)
+        st = mbs.sgd_state(0.05, 0.9, 5e-4)
+        acc = mbs.GradientAccumulator(params)
+        res = d.train_epoch(net, xs, ys, mini_batch_size=mini, micro_batch_size=n_mu,
+                            normalization="exact_weighted", loss_kind="cross_entropy", optimizer_state=st, seed=4,
+                            epoch_index=1, accumulator=acc, prefetch=True)      # host shard: streamed
+        q.put((rank, params.flat.cpu().numpy().copy(), [r.loss for r in res], st.step_count))
+        dist.barrier()
+        if d.peer is not None:
+            d.peer.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_dp_train_epoch_weak_scaling(cuda, transport):
+    """Each rank streams its own host shard in its own order; == single process on the united mini-batches."""
+    import paper_2110_12484_b200 as mbs
+    world, shard, mini, n_mu = 2, 24, 12, 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_epoch, args=(r, world, port, shard, mini, n_mu, q, transport))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    np.testing.assert_array_equal(res[0][1], res[1][1])
+    assert res[0][3] == shard // mini
+    # single process: global mini-batch m = concat_r shard_r[order_r[m*mini:(m+1)*mini]]
+    x, y = _data(shard * world)
+    orders = [mbs.named_stream(4, f"shuffle/epoch1/rank{r}").permutation(shard) for r in range(world)]
+    dev = torch.device("cuda:0")
+    net = _net().to(dev)
+    params = mbs.ParameterSet(net)
+    st = mbs.sgd_state(0.05, 0.9, 5e-4)
+    acc = mbs.GradientAccumulator(params)
+    losses = []
+    for m in range(shard // mini):
+        idx = np.concatenate([r * shard + orders[r][m * mini:(m + 1) * mini] for r in range(world)])
+        ii = torch.from_numpy(idx.astype(np.int64))
+        _, s = mbs.train_mini_batch(net, params, (x[ii].to(dev), y[ii].to(dev)),
+                                    mbs.plan_split(world * mini, n_mu), "exact_weighted", "cross_entropy", st,
+                                    accumulator=acc)
+        losses.append(s.loss)
+    w = params.flat.cpu().numpy()
+    assert np.linalg.norm(res[0][1] - w) / np.linalg.norm(w) <= 1e-6
+    np.testing.assert_allclose(res[0][2], losses, rtol=1e-5)

@@ -1,5 +1,9 @@
 """Isolated MBS kernel microbenchmarks (L2 flushed between launches), C2 / C3 layouts.
 
+The flush READS a 512 MB buffer (L2 ends up full of clean lines): a write-flush
+would leave ~126 MB of dirty lines whose write-back lands inside the next timed
+kernel (19 us of extra traffic at 6.5 TB/s). ``--flush write`` keeps that mode.
+
 python tools/kbench.py [--config c2] -> JSON with algorithmic GB/s per kernel.
 """
 import argparse
@@ -17,20 +21,25 @@ from paper_2110_12484_b200.workloads import WORKLOADS, build_model  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--flush", default="read", choices=["read", "write"])
 args = ap.parse_args()
 w = WORKLOADS[args.config]
 dev = torch.device("cuda:0")
 model = build_model(w).to(dev).to(memory_format=torch.channels_last)
 params = mbs.ParameterSet(model)
 P = params.layout.n_params
-flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)
+flush = torch.ones(128 * 2 ** 20, dtype=torch.float32, device=dev)
+flush_sink = torch.empty((), dtype=torch.float32, device=dev)
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
 
 
 def timeit(fn, nbytes):
     ts = []
     for i in range(args.iters + 3):
-        flush.fill_(i & 0xFF)
+        if args.flush == "write":
+            flush.fill_(float(i))
+        else:
+            torch.sum(flush, dim=(0,), out=flush_sink)
         torch.cuda._sleep(2_000_000)      # GPU busy ~1 ms: host-side launch overhead is off the clock
         s, e = torch.cuda.Event(True), torch.cuda.Event(True)
         s.record()
@@ -45,7 +54,7 @@ def timeit(fn, nbytes):
             "frac": nbytes / (med / 1e3) / 1e9 / peak, "bytes": nbytes}
 
 
-out = {"P": P, "segments": len(params.layout.names), "peak_gbs": peak}
+out = {"P": P, "segments": len(params.layout.names), "peak_gbs": peak, "flush": args.flush}
 acc = mbs.GradientAccumulator(params)
 grads = [torch.randn(s, device=dev).contiguous(memory_format=torch.channels_last) if len(s) == 4 else
          torch.randn(s, device=dev) for s in params.layout.shapes]
