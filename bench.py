@@ -361,7 +361,7 @@ def main():
                        "l2": ("inputs > L2: every mini-batch is %.0f MB of uint8" % (x_dev[:n_b].numel() / 1e6)) +
                              ", none reused within the timed region",
                        "api": ("engine.train_epoch" if ws == 1 else "dp.DataParallelMBS.train_epoch (per-rank "
-                               "shards, one NCCL all-reduce per global mini-batch)") +
+                               "shards, one all-reduce per global mini-batch, transport=%s)" % dp.transport) +
                               " over `steps` shuffled mini-batches",
                        "autosize": autosize},
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": int(h2d_bytes),

@@ -55,10 +55,23 @@ struct GradPtrs {
 };
 
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
+#if defined(MBS_K1_PLAIN_G)
+    return __ldg(p);
+#else
     float4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
                  : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
     return r;
+#endif
+}
+
+// the accumulator is read then written by the same thread only: the non-coherent path is safe
+__device__ __forceinline__ float4 ld_acc(const float4* p) {
+#if defined(MBS_K1_NC_ACC)
+    return __ldg(p);
+#else
+    return *p;
+#endif
 }
 
 __device__ __forceinline__ double sq4(float4 a) {
@@ -108,7 +121,7 @@ __device__ __forceinline__ void accum_piece(float* __restrict__ a, const float* 
                 const int i = base + u * kThreads;
                 if (i < n4) {
                     gv[u] = ld_stream(g4 + i);
-                    if (!ASSIGN) av[u] = a4[i];
+                    if (!ASSIGN) av[u] = ld_acc(a4 + i);
                 }
             }
 #pragma unroll
