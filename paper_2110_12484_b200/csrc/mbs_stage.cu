@@ -274,13 +274,210 @@ k_stage_nhwc_smem(const TI* __restrict__ src, const int64_t* __restrict__ rows, 
     }
 }
 
-static int stage_path() {
-    static int path = -1;
-    if (path < 0) {
-        const char* e = getenv("MBS_K2_PATH");   // A/B only: 0 = per-row, 1 = grid-stride vec, 2 = smem (default)
-        path = e ? atoi(e) : 2;
+// ---------------------------------------------------------------------------------------------
+// NCHW u8 -> NHWC through the bulk-async copy engine (TMA, cp.async.bulk), persistent CTAs.
+//
+// Each CTA walks tiles t = blockIdx.x, +grid, ... of TP pixels of one row. One elected thread
+// keeps S tiles of source planes in flight (one 1-D bulk copy per channel plane into a ring of
+// S smem stages, completion counted in bytes on the stage's mbarrier). All threads convert a
+// landed stage to the interleaved NHWC tile in one of two smem output buffers, and the elected
+// thread sends it with ONE bulk store (smem -> global, bulk_group). So a CTA always has loads of
+// the next tiles and the store of the previous tile outstanding while it converts the current
+// one, without per-thread register staging; grid = resident CTAs (a multiple of the SM count).
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+constexpr int kBulkStages = 3;
+
+template <int TP, int C, typename TO>
+constexpr size_t bulk_smem_bytes() {
+    return (size_t)kBulkStages * C * TP + 2 * (size_t)TP * C * sizeof(TO);
+}
+
+template <int OUT, int C, int TP>
+__global__ void __launch_bounds__(kStageThreads)
+k_stage_nhwc_bulk(const uint8_t* __restrict__ src, const int64_t* __restrict__ rows, int64_t row0, int64_t HW,
+                  int64_t tiles_per_row, int64_t total_tiles, typename Out<OUT>::T* __restrict__ dst) {
+    using TO = typename Out<OUT>::T;
+    constexpr int PX = TP / kStageThreads;                // pixels per thread in the conversion
+    static_assert(PX == 8 || PX == 16, "tile must give 8 or 16 pixels per thread");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[kBulkStages];
+    uint8_t* in = smem_raw;                                             // [S][C][TP] source planes
+    TO* out = reinterpret_cast<TO*>(smem_raw + (size_t)kBulkStages * C * TP);   // [2][TP*C] NHWC tiles
+    const int tid = threadIdx.x;
+    const int64_t G = gridDim.x;
+    const int64_t n_mine = total_tiles > (int64_t)blockIdx.x ? (total_tiles - blockIdx.x + G - 1) / G : 0;
+
+    auto tile_of = [&](int64_t i, int64_t& r, int64_t& p0, int& npx) {
+        const int64_t t = blockIdx.x + i * G;
+        r = t / tiles_per_row;
+        p0 = (t - r * tiles_per_row) * TP;
+        npx = (int)min((int64_t)TP, HW - p0);
+    };
+    auto issue = [&](int64_t i) {                         // elected thread: tile i's planes -> stage i % S
+        int64_t r, p0;
+        int npx;
+        tile_of(i, r, p0, npx);
+        const int s = (int)(i % kBulkStages);
+        const uint8_t* base = src + src_row(rows, row0, r) * (int64_t)C * HW + p0;
+        mbar_expect_tx(&full[s], (uint32_t)(C * npx));
+#pragma unroll
+        for (int c = 0; c < C; ++c) bulk_load(in + ((size_t)s * C + c) * TP, base + c * HW, (uint32_t)npx, &full[s]);
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < kBulkStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int64_t i = 0; i < min((int64_t)kBulkStages, n_mine); ++i) issue(i);
     }
-    return path;
+    __syncthreads();
+
+    for (int64_t i = 0; i < n_mine; ++i) {
+        int64_t r, p0;
+        int npx;
+        tile_of(i, r, p0, npx);
+        const int s = (int)(i % kBulkStages);
+        const int ob = (int)(i & 1);
+        TO* o = out + (size_t)ob * TP * C;
+        if (tid == 0) bulk_wait_read<1>();                // the store of tile i-2 has finished reading out[ob]
+        mbar_wait(&full[s], (uint32_t)((i / kBulkStages) & 1));
+        __syncthreads();
+        const uint8_t* pl = in + (size_t)s * C * TP;
+        const int q0 = tid * PX;
+        if (q0 + PX <= npx) {
+            uint32_t w[C][PX / 4];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                if constexpr (PX == 16) {
+                    const uint4 q = *reinterpret_cast<const uint4*>(pl + c * TP + q0);
+                    w[c][0] = q.x; w[c][1] = q.y; w[c][2] = q.z; w[c][3] = q.w;
+                } else {
+                    const uint2 q = *reinterpret_cast<const uint2*>(pl + c * TP + q0);
+                    w[c][0] = q.x; w[c][1] = q.y;
+                }
+            }
+            constexpr int per = 16 / (int)sizeof(TO);     // outputs per 16-byte smem store
+            uint4* d16 = reinterpret_cast<uint4*>(o + (size_t)q0 * C);
+#pragma unroll
+            for (int v = 0; v < PX * C / per; ++v) {
+                TO e[per];
+#pragma unroll
+                for (int j = 0; j < per; ++j) {
+                    const int k = v * per + j, px = k / C, c = k % C;
+                    e[j] = Out<OUT>::cvt((float)((w[c][px >> 2] >> ((px & 3) * 8)) & 0xFFu));
+                }
+                uint4 q;
+                memcpy(&q, e, 16);
+                d16[v] = q;
+            }
+        } else {
+            for (int q = q0; q < npx && q < q0 + PX; ++q)
+                for (int c = 0; c < C; ++c) o[q * C + c] = Out<OUT>::cvt((float)pl[c * TP + q]);
+        }
+        fence_proxy_async_smem();                          // generic-proxy smem writes -> visible to the bulk store
+        __syncthreads();                                   // stage s consumed, out[ob] complete
+        if (tid == 0) {
+            bulk_store(dst + (r * HW + p0) * C, o, (uint32_t)(npx * C * sizeof(TO)));
+            if (i + kBulkStages < n_mine) issue(i + kBulkStages);
+        }
+    }
+    if (tid == 0) bulk_wait_all();
+}
+
+static int stage_path() {
+    // A/B only: 0 = per-row, 1 = grid-stride vec, 2 = smem, 3 = bulk-async (default)
+    const char* e = getenv("MBS_K2_PATH");
+    return e ? atoi(e) : 3;
+}
+
+static int bulk_tile() {
+    const char* e = getenv("MBS_K2_TILE");   // A/B only: 2048 (default) or 4096 pixels per tile
+    return (e && atoi(e) == 4096) ? 4096 : 2048;
+}
+
+static bool is_device_memory(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice;
+}
+
+static int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <int OUT, int C, int TP>
+static int launch_bulk(const uint8_t* s, const int64_t* rows, int64_t row0, int64_t n_rows, int64_t HW,
+                       typename Out<OUT>::T* d, cudaStream_t st) {
+    using TO = typename Out<OUT>::T;
+    auto kern = k_stage_nhwc_bulk<OUT, C, TP>;
+    constexpr size_t sm = bulk_smem_bytes<TP, C, TO>();
+    static int per_sm = 0;                                 // resident CTAs per SM (per template instance)
+    if (!per_sm) {
+        MBS_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        MBS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStageThreads, sm));
+        if (per_sm < 1) per_sm = 1;
+    }
+    const int64_t tpr = (HW + TP - 1) / TP, total = n_rows * tpr;
+    const int grid = (int)std::min<int64_t>(total, (int64_t)sm_count() * per_sm);
+    kern<<<grid, kStageThreads, sm, st>>>(s, rows, row0, HW, tpr, total, d);
+    MBS_CK_LAUNCH("k_stage_nhwc_bulk");
+    return MBS_OK;
 }
 
 static int resident_grid(int64_t units) {
@@ -332,7 +529,21 @@ static int stage_typed(const void* src, const int64_t* rows, int64_t row0, int64
         const bool plane_ok = (HW % kPix == 0) && ((HW * (int64_t)sizeof(TI)) % 16 == 0) && (sa % 16 == 0) &&
                               (da % 16 == 0) && ((kPix * sizeof(TO)) % 16 == 0);
         const int path = stage_path();
-        if (path == 2 && nhwc && C <= 4 && (HW * (int64_t)sizeof(TI)) % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
+        if constexpr (sizeof(TI) == 1) {
+            if (path == 3 && nhwc && C <= 4 && HW % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
+                is_device_memory(src)) {
+                const bool small = OUT == MBS_F32 || bulk_tile() == 2048;   // f32 tiles: 2048 px keeps 2 CTAs/SM
+                switch (C) {
+                    case 2: return small ? launch_bulk<OUT, 2, 2048>(s, rows, row0, n_rows, HW, d, st)
+                                         : launch_bulk<OUT, 2, 4096>(s, rows, row0, n_rows, HW, d, st);
+                    case 3: return small ? launch_bulk<OUT, 3, 2048>(s, rows, row0, n_rows, HW, d, st)
+                                         : launch_bulk<OUT, 3, 4096>(s, rows, row0, n_rows, HW, d, st);
+                    default: return small ? launch_bulk<OUT, 4, 2048>(s, rows, row0, n_rows, HW, d, st)
+                                          : launch_bulk<OUT, 4, 4096>(s, rows, row0, n_rows, HW, d, st);
+                }
+            }
+        }
+        if ((path == 2 || path == 3) && nhwc && C <= 4 && (HW * (int64_t)sizeof(TI)) % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
             ((int64_t)kTilePx * C * sizeof(TO)) % 16 == 0 && (HW * C * (int64_t)sizeof(TO)) % 16 == 0) {
             const int64_t tpr = (HW + kTilePx - 1) / kTilePx, total = n_rows * tpr;
             const size_t sm = (size_t)kTilePx * C * sizeof(TO);

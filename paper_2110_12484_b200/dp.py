@@ -17,8 +17,10 @@ rank (at most one micro-batch of imbalance). Each rank:
     — or, with ``transport="peer"``, runs the last K1 and the
    all-reduce as ONE kernel over CUDA-IPC peer memory (K1C, ``mbs_peer.cu``);
 3. after the last bucket, recomputes the grad norm of the reduced sum (the
-   optimizer's non-finite guard), all-reduces the tiny loss record, and runs
-   the identical K3 step on every rank.
+   optimizer's non-finite guard), all-reduces the tiny loss record, merges the
+   BN running statistics so they equal the single-device sequential ones
+   (``BNStatSync``, one small all-reduce), and runs the identical K3 step on
+   every rank.
 
 The pure functions (partition, factors, buckets, stats combination) carry the
 logic and are exercised on CPU with the gloo backend (tests/test_dp_gloo.py).
@@ -97,6 +99,89 @@ def combine_loss_record(losses_local: list, factors_local: list, weights_local: 
         v[1 + n_s_mu + k0 + j] = l * f
     v[0] /= n_b
     return v
+
+
+def bn_merge_coefficients(momentum, block: tuple, n_s_mu: int) -> tuple:
+    """Coefficients that turn per-rank BN running statistics into the single-device sequential ones.
+
+    torch BN (and the reference, ``nn.py:329-332``) updates a running statistic
+    once per micro-batch, r <- (1-m) r + m s_k, in plan order. Starting every
+    rank from the same r0, rank r's block of n_r micro-batches ends at
+    R_r = c^n_r r0 + L_r (c = 1-m, L_r its own terms), and the single-device
+    run over all K micro-batches ends at c^K r0 + sum_r c^(K-k1_r) L_r. So the
+    exchange is ONE SUM all-reduce of contrib_r = a (R_r - b r0), followed by
+    R = g r0 + sum, with (a, b, g) = (c^(K-k1_r), c^n_r, c^K) returned here.
+    ``momentum=None`` (cumulative average) is handled on device by the caller.
+    """
+    k0, k1 = block
+    c = 1.0 - float(momentum)
+    return c ** (n_s_mu - k1), c ** (k1 - k0), c ** n_s_mu
+
+
+class BNStatSync:
+    """Makes data-parallel BN running statistics equal the single-device MBS run.
+
+    Each rank sees only its own micro-batches, so without this its
+    ``running_mean/var`` follow a different EMA than the single-device run.
+    ``snapshot()`` before the rank's first micro-batch forward, ``merge()``
+    after its last: one SUM all-reduce of a flat buffer of every BN running
+    statistic (ResNet-50: 53 layers, 53,120 values) recovers the sequential
+    single-device statistics exactly up to fp32 rounding, and
+    ``num_batches_tracked`` advances by the GLOBAL micro-batch count.
+    """
+
+    def __init__(self, model: torch.nn.Module, dist, group=None):
+        bn = torch.nn.modules.batchnorm._BatchNorm
+        self.mods = [m for m in model.modules()
+                     if isinstance(m, bn) and m.track_running_stats and m.running_mean is not None]
+        self.dist, self.group = dist, group
+        self._coef = {}
+        self._r0 = None
+        self._n0 = None
+
+    def _bufs(self):
+        return [t for m in self.mods for t in (m.running_mean, m.running_var)]
+
+    def snapshot(self):
+        if not self.mods:
+            return
+        with torch.no_grad():
+            self._r0 = torch.cat([t.reshape(-1) for t in self._bufs()])
+            self._n0 = torch.stack([m.num_batches_tracked for m in self.mods])
+
+    def merge(self, block: tuple, n_s_mu: int):
+        """contrib = A*local - B*r0 (SUM-all-reduced), then r = (G*r0 + sum) * D, per BN layer:
+        EMA layers (a, a*b, g, 1) from ``bn_merge_coefficients``; cumulative-average layers
+        (n0+n_r, n0, n0, 1/(n0+K)) with n0 = num_batches_tracked before the step (on device)."""
+        if not self.mods:
+            return
+        with torch.no_grad():
+            r0 = self._r0
+            dev, dt = r0.device, r0.dtype
+            n_r = block[1] - block[0]
+            key = (block, n_s_mu)
+            if key not in self._coef:
+                ema = [bn_merge_coefficients(m.momentum if m.momentum is not None else 0.0, block, n_s_mu)
+                       for m in self.mods]
+                host = torch.tensor([[a, a * b, g, 1.0] for a, b, g in ema], dtype=torch.float64)
+                cma = torch.tensor([m.momentum is None for m in self.mods])
+                counts = torch.tensor([2 * m.running_mean.numel() for m in self.mods])
+                self._coef[key] = (host.to(dev), cma.to(dev), counts.to(dev), bool(cma.any()))
+            host, cma, counts, any_cma = self._coef[key]
+            coef = host
+            if any_cma:
+                n0 = self._n0.double()
+                alt = torch.stack([n0 + n_r, n0, n0, 1.0 / (n0 + n_s_mu)], dim=1)
+                coef = torch.where(cma[:, None], alt, host)
+            A, B, G, D = torch.repeat_interleave(coef.to(dt), counts, dim=0).unbind(1)
+            local = torch.cat([t.reshape(-1) for t in self._bufs()])
+            contrib = A * local - B * r0
+            self.dist.all_reduce(contrib, group=self.group)
+            new = (G * r0 + contrib) * D
+            bufs = self._bufs()
+            torch._foreach_copy_(bufs, [p.view_as(t) for p, t in zip(new.split([t.numel() for t in bufs]), bufs)])
+            for m, n0 in zip(self.mods, self._n0):
+                m.num_batches_tracked.copy_(n0 + n_s_mu)
 
 
 class _Result:
@@ -178,10 +263,15 @@ class DataParallelMBS:
     and the all-reduce are ONE kernel over peer memory (``PeerExchange``, K1C).
     """
 
-    def __init__(self, params: ParameterSet, process_group=None, bucket_mb: float = 32.0, transport: str = "nccl"):
+    def __init__(self, params: ParameterSet, process_group=None, bucket_mb: float = 32.0, transport: str = "nccl",
+                 bn_stats: str = "sequential"):
         import torch.distributed as dist
         if transport not in ("nccl", "peer"):
             raise ValueError(f"unknown transport {transport!r}")
+        if bn_stats not in ("sequential", "local"):
+            raise ValueError(f"unknown bn_stats mode {bn_stats!r}")
+        self.bn_stats = bn_stats
+        self._bn = {}
         self.dist = dist
         self.params = params
         self.group = process_group
@@ -288,6 +378,12 @@ class DataParallelMBS:
         acc.begin(n_local)
         ctx = torch.autocast("cuda", dtype=autocast_dtype) if autocast_dtype is not None else nullcontext()
         model.train()
+        bn = None
+        if self.bn_stats == "sequential" and self.world > 1:
+            bn = self._bn.get(id(model))
+            if bn is None:
+                bn = self._bn[id(model)] = BNStatSync(model, self.dist, self.group)
+            bn.snapshot()
         losses, factors, weights = [], [], []
         works = []
         plist = acc._plist
@@ -371,6 +467,8 @@ class DataParallelMBS:
             rec[1 + k0:1 + k0 + n_local] = lv
             rec[1 + plan.n_s_mu + k0:1 + plan.n_s_mu + k0 + n_local] = lv * fv
         self.dist.all_reduce(rec, group=self.group)
+        if bn is not None:
+            bn.merge(block, plan.n_s_mu)
         total = acc.as_gradient_set()
         if lr_for_step is not None:
             optimizer_state.lr = lr_for_step(optimizer_state.step_count)

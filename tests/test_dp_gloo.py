@@ -125,3 +125,75 @@ def test_partition_and_buckets():
     assert dp.local_factors(p2, (5, 6), "exact_weighted") == [16 / 256]
     with pytest.raises(ValueError):
         dp.weak_scaling_plan(100, 48, 2)
+
+
+def _bn_model():
+    torch.manual_seed(11)
+    return torch.nn.Sequential(torch.nn.Conv2d(3, 6, 3, padding=1), torch.nn.BatchNorm2d(6, momentum=0.1),
+                               torch.nn.ReLU(), torch.nn.Conv2d(6, 4, 3, padding=1),
+                               torch.nn.BatchNorm2d(4, momentum=0.3), torch.nn.Flatten(),
+                               torch.nn.Linear(4 * 8 * 8, 5), torch.nn.BatchNorm1d(5, momentum=None))
+
+
+BN_CASES = [(20, 4), (17, 3), (9, 9)]        # even split, ragged tail, one micro-batch (idle ranks)
+
+
+def _bn_worker(rank, world, port, steps, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.set_num_threads(1)
+        out = []
+        for n_b, n_mu in BN_CASES:
+            net = _bn_model().double().train()
+            x = torch.from_numpy(_data(n_b * steps)[0])
+            plan = O.plan_split(n_b, n_mu)
+            block = dp.partition_micro_batches(plan, world)[rank]
+            sync = dp.BNStatSync(net, dist)
+            with torch.no_grad():
+                for s in range(steps):
+                    sync.snapshot()
+                    for k in range(*block):
+                        lo, hi = plan.index_ranges[k]
+                        net(x[s * n_b + lo:s * n_b + hi])
+                    sync.merge(block, plan.n_s_mu)
+            out.append({k: v.clone().numpy() for k, v in net.state_dict().items() if "running" in k or "tracked" in k})
+        out_q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bn_running_stats_match_single_device():
+    """DP BN running stats (momentum EMA and cumulative average) == the sequential single-device micro loop."""
+    world, steps = 3, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bn_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for case, (n_b, n_mu) in enumerate(BN_CASES):
+        net = _bn_model().double().train()
+        x = torch.from_numpy(_data(n_b * steps)[0])
+        plan = O.plan_split(n_b, n_mu)
+        with torch.no_grad():
+            for s in range(steps):
+                for lo, hi in plan.index_ranges:
+                    net(x[s * n_b + lo:s * n_b + hi])
+        want = {k: v.numpy() for k, v in net.state_dict().items() if "running" in k or "tracked" in k}
+        for _, got_all in res:
+            got = got_all[case]
+            assert set(got) == set(want)
+            for k in want:
+                np.testing.assert_allclose(got[k], want[k], rtol=1e-12, atol=1e-13, err_msg=f"{n_b}/{n_mu} {k}")
+
+
+def test_bn_merge_coefficients():
+    c = 0.9
+    assert dp.bn_merge_coefficients(0.1, (2, 5), 8) == pytest.approx((c ** 3, c ** 3, c ** 8))
+    assert dp.bn_merge_coefficients(0.1, (5, 5), 8) == pytest.approx((c ** 3, 1.0, c ** 8))

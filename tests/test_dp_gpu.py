@@ -59,12 +59,17 @@ def _rank(rank, world, port, backend, n_per_rank, n_mu, mode, q):
             r = d.train_mini_batch(net, (xs.to(dev), ys.to(dev)), n_per_rank, n_mu, mode, "cross_entropy", st,
                                    accumulator=acc)
             out.append((r.loss, list(r.losses_raw), r.grad_norm, r.step_count))
-        q.put((rank, params.flat.cpu().numpy().copy(), out, len(d.buckets)))
+        q.put((rank, params.flat.cpu().numpy().copy(), out, len(d.buckets), _bn_state(net)))
     finally:
         dist.destroy_process_group()
 
 
-def _single(n_b, n_mu, mode, steps=2):
+def _bn_state(net):
+    return {k: v.detach().cpu().double().numpy().copy() for k, v in net.state_dict().items()
+            if "running" in k or "tracked" in k}
+
+
+def _single(n_b, n_mu, mode, steps=2, with_bn=False):
     import paper_2110_12484_b200 as mbs
     torch.backends.cudnn.allow_tf32 = False
     dev = torch.device("cuda:0")
@@ -78,6 +83,8 @@ def _single(n_b, n_mu, mode, steps=2):
         _, s = mbs.train_mini_batch(net, params, (x.to(dev), y.to(dev)), mbs.plan_split(n_b, n_mu), mode,
                                     "cross_entropy", st, accumulator=acc)
         out.append((s.loss, list(s.losses_raw), s.grad_norm, s.step_count))
+    if with_bn:
+        return params.flat.cpu().numpy(), out, _bn_state(net)
     return params.flat.cpu().numpy(), out
 
 
@@ -101,9 +108,13 @@ def test_two_ranks_share_one_gpu_gloo(cuda, mode):
     res = _run(2, "gloo", n_per_rank, n_mu, mode)
     assert res[0][3] > 1
     np.testing.assert_array_equal(res[0][1], res[1][1])           # every rank steps identically
-    w_single, out_single = _single(2 * n_per_rank, n_mu, mode)
+    w_single, out_single, bn_single = _single(2 * n_per_rank, n_mu, mode, with_bn=True)
     err = np.linalg.norm(res[0][1] - w_single) / np.linalg.norm(w_single)
     assert err <= 1e-6, err
+    # BN running statistics merged by BNStatSync == the single-device sequential micro loop (fp32 rounding)
+    for k, v in bn_single.items():
+        for r in range(2):
+            np.testing.assert_allclose(res[r][4][k], v, rtol=1e-5, atol=1e-6, err_msg=k)
     for (l, raw, gn, sc), (l1, raw1, gn1, sc1) in zip(res[0][2], out_single):
         assert sc == sc1
         assert l == pytest.approx(l1, rel=1e-5)

@@ -56,6 +56,27 @@ def test_stage_bit_exact(cuda, src_dtype, dst_dtype, shape, cl):
     assert torch.equal(_bits(got2), _bits(want2))
 
 
+@pytest.mark.parametrize("path", ["0", "1", "2", "3", "3:2048"])
+@pytest.mark.parametrize("dst_dtype", [torch.float32, torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("shape", [(9, 3, 80, 80), (5, 3, 224, 224), (7, 4, 64, 64), (6, 2, 48, 48),
+                                   (300, 3, 16, 16)])
+def test_stage_u8_nhwc_every_path(cuda, monkeypatch, path, dst_dtype, shape):
+    """Every K2 NHWC implementation (MBS_K2_PATH: per-row, grid-stride, smem tile, bulk-async TMA ring) is
+    bit-exact, including ragged last tiles (80x80 = 4096 + 2304 px, 224x224 = 12 x 4096 + 1024 px) and
+    more tiles than resident CTAs."""
+    monkeypatch.setenv("MBS_K2_PATH", path.split(":")[0])
+    monkeypatch.setenv("MBS_K2_TILE", path.split(":")[-1])
+    x = _src(torch.uint8, shape, cuda)
+    rows = torch.from_numpy(O.epoch_order(shape[0], 5, 2).astype(np.int64)).to(cuda)
+    st = Staging(dtype=dst_dtype, channels_last=True)
+    got = stage_rows(x, torch.uint8, tuple(shape[1:]), rows, 0, len(rows), st, cuda)
+    want = x[rows].to(dst_dtype).contiguous(memory_format=torch.channels_last)
+    assert torch.equal(_bits(got), _bits(want))
+    got2 = stage_rows(x, torch.uint8, tuple(shape[1:]), None, 1, shape[0] - 2, st, cuda)
+    want2 = x[1:shape[0] - 1].to(dst_dtype).contiguous(memory_format=torch.channels_last)
+    assert torch.equal(_bits(got2), _bits(want2))
+
+
 def test_stage_bf16_rounding_matches_torch(cuda):
     # ties-to-even and NaN handling of f32 -> bf16
     vals = torch.tensor([1.00390625, 1.01171875, -2.5e-39, float("nan"), float("inf"), -float("inf"), 3.0e38,
