@@ -158,6 +158,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=16, help="samples per CPU-reference step")
+    ap.add_argument("--model-bn", default="k5", choices=["k5", "torch"],
+                    help="the model's BatchNorm(+ReLU/+residual): K5 sm_100a kernels or stock torch")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -203,7 +205,7 @@ def main():
     torch.backends.cudnn.benchmark = True
     torch.manual_seed(1234 + rank)
 
-    model = build_model(w).to(dev).to(memory_format=torch.channels_last)
+    model = build_model(w, bn=args.model_bn).to(dev).to(memory_format=torch.channels_last)
     params = mbs.ParameterSet(model)
     staging = Staging(dtype=torch.bfloat16, channels_last=True)
     autocast = torch.bfloat16
@@ -296,6 +298,14 @@ def main():
         ms_dev, _ = timed(False, args.steps, args.warmup, k1_timer=True)
     kstats = TIMER.summary()
     launches_value = TIMER.launches
+    # K5 (model BatchNorm) bandwidth: one more HBM-resident mini-batch with its launches timed (not in `value`)
+    k5stats = {}
+    if args.model_bn == "k5":
+        TIMER.reset()
+        TIMER.enabled = TIMER.k5 = True
+        epoch(False, 1, 2000, warm_mini)
+        TIMER.enabled = TIMER.k5 = False
+        k5stats = {k: v for k, v in TIMER.summary().items() if k.startswith("k5_")}
     samples_total = n_b * args.steps * ws
     value = samples_total / (ms_dev / 1e3)
 
@@ -312,7 +322,9 @@ def main():
     streamer.close()
 
     # --- no-stream baseline: plain torch training at batch = micro, data resident ---
-    nos = no_stream_baseline(w, dev, n_mu, args.steps, args.warmup, ws)
+    nos = no_stream_baseline(w, dev, n_mu, args.steps, args.warmup, ws, bn=args.model_bn)
+    nos_torch = (no_stream_baseline(w, dev, n_mu, args.steps, args.warmup, ws, bn="torch")
+                 if args.model_bn != "torch" else None)
 
     # the reference's overhead report (streaming.py:130-149) on MEASURED schedules: the MBS step as
     # run (copy per micro from the streamer's events, compute per micro from the timed step) vs the
@@ -348,6 +360,18 @@ def main():
                               "(acc = s*g); P = %d" % params.layout.n_params,
                 "other_kernels": {k: {"gbs": v["gbs"], "avg_us": v["avg_ms"] * 1e3, "launches": v["launches"]}
                                   for k, v in kstats.items() if k != "k1_accumulate"}}
+    roofline_k5 = None
+    if k5stats:
+        kb = sum(v["bytes_per_launch"] * v["launches"] for v in k5stats.values())
+        kt = sum(v["total_ms"] for v in k5stats.values())
+        roofline_k5 = {"kernel": "k5 micro-batch BatchNorm (+ReLU/+residual), forward and backward",
+                       "bound": "hbm", "achieved": kb / (kt / 1e3) / 1e9, "peak": peak, "peak_kind": peak_kind,
+                       "unit": "GB/s", "frac": kb / (kt / 1e3) / 1e9 / peak,
+                       "ms_per_mini_batch": kt, "calls": {k: v["launches"] for k, v in k5stats.items()},
+                       "per_call": {k: {"gbs": v["gbs"], "avg_us": v["avg_ms"] * 1e3} for k, v in k5stats.items()},
+                       "bytes_rule": "per call over E activation elements of s bytes: forward 3*E*s (+E*s "
+                                     "residual), backward 5*E*s (+3*E*s residual); CUDA events around each "
+                                     "3-kernel call, so small layers include launch gaps"}
 
     line = {"metric": "effective-batch samples/sec", "value": value, "unit": "samples/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev / args.steps,
@@ -357,6 +381,8 @@ def main():
                        "n_micro": plan.n_s_mu, "global_batch": n_b * ws, "parallelism": f"dp{ws}",
                        "normalization": w.normalization, "optimizer": w.optimizer,
                        "model_precision": "bf16 autocast on cuDNN/cuBLAS, fp32 master weights; MBS path fp32",
+                       "model_bn": ("BatchNorm(+ReLU/+residual) on K5 sm_100a kernels (bn.py), micro-batch "
+                                    "statistics" if args.model_bn == "k5" else "stock torch BatchNorm"),
                        "input": "uint8 NCHW staged to bf16 NHWC by K2",
                        "l2": ("inputs > L2: every mini-batch is %.0f MB of uint8" % (x_dev[:n_b].numel() / 1e6)) +
                              ", none reused within the timed region",
@@ -368,6 +394,7 @@ def main():
                     "d2h_bytes_per_step": 8 * (4 + 2 * plan.n_s_mu), "ms_per_step": ms_host / args.steps},
             "h2d_overlap_pct": overlap, "h2d_gbs": h2d_gbs, "accum_gbs": k1.get("gbs"),
             "no_stream": nos, "stream_vs_no_stream": value / nos["value"] if nos else None, "overhead": overhead,
+            "no_stream_torch_bn": nos_torch, "roofline_k5": roofline_k5,
             "e2e_vs_no_stream": e2e / nos["value"] if nos else None,
             "roofline": roofline, "gpu_launches": launches_value, "gpu_launches_e2e": launches_e2e,
             "clocks": clocks.summary(), "final_loss": losses[-1] if losses else None}
@@ -385,12 +412,14 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def no_stream_baseline(w, dev, batch, steps, warmup, ws):
-    """The paper's 'w/o MBS' run: plain torch training, batch = micro-batch, data resident in HBM."""
+def no_stream_baseline(w, dev, batch, steps, warmup, ws, bn="torch"):
+    """The paper's 'w/o MBS' run: plain torch training, batch = micro-batch, data resident in HBM.
+
+    ``bn`` selects the same model definition as the MBS run (K5 or stock torch BatchNorm)."""
     from paper_2110_12484_b200.losses import compute_loss
     from paper_2110_12484_b200.workloads import build_model, synthetic_data
     torch.manual_seed(0)
-    model = build_model(w).to(dev).to(memory_format=torch.channels_last)
+    model = build_model(w, bn=bn).to(dev).to(memory_format=torch.channels_last)
     if w.optimizer == "sgd":
         opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9, weight_decay=5e-4, fused=True)
     else:
@@ -421,7 +450,8 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws):
     ms = e0.elapsed_time(e1)
     del model, opt
     return {"value": batch * n * ws / (ms / 1e3), "unit": "samples/s", "batch": batch,
-            "steps": n, "how": "torch fwd/bwd + fused torch.optim step per batch, bf16 autocast, data in HBM"}
+            "steps": n, "model_bn": bn,
+            "how": "torch fwd/bwd + fused torch.optim step per batch, bf16 autocast, data in HBM"}
 
 
 if __name__ == "__main__":

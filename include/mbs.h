@@ -220,6 +220,34 @@ int mbs_accum_add_allreduce(mbs_accum_t h, mbs_peer_t peer, const float* const* 
                             const float* loss_dev, double loss_factor, double loss_weight,
                             double timeout_ms, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Micro-batch BatchNorm (K5) — the model-side op of every micro-batch forward
+ * in training mode: statistics over the MICRO-batch (reference nn.py:275-282
+ * BatchNorm2d.forward, biased variance for the normalisation), one
+ * running-statistics update per micro-batch (nn.py:329-332; torch's unbiased
+ * running_var convention), fused with the ReLU that follows it and, for
+ * residual blocks, the skip add before that ReLU: y = relu(bn(x) [+ residual]).
+ *
+ * x / residual / y / dy / dx / dresidual are channels-last activations:
+ * `rows` (= N*H*W) x `C` row-major, dtype MBS_BF16 or MBS_F32. weight/bias
+ * (may be NULL: 1 / 0), running stats (both NULL: not tracked), save_* and
+ * dweight/dbias are fp32 [C]. `workspace` is device scratch of at least
+ * mbs_bn_workspace_bytes() bytes, exclusively owned by the call until it has
+ * executed on `stream`. A residual is only accepted together with relu=1.
+ * Deterministic: fixed-order reductions, no atomics.
+ * ------------------------------------------------------------------------- */
+int mbs_bn_workspace_bytes(int64_t rows, int64_t C, int dtype, int64_t* bytes);
+int mbs_bn_forward(const void* x, const void* residual, void* y, int dtype, int64_t rows, int64_t C,
+                   const float* weight, const float* bias, float* running_mean, float* running_var,
+                   double momentum, double eps, int relu, float* save_mean, float* save_invstd,
+                   void* workspace, void* stream);
+/* Gradients of mbs_bn_forward: dx, dresidual (iff residual), dweight/dbias (may be NULL).
+ * The ReLU mask is recomputed from x (and residual) bit-identically to the forward. */
+int mbs_bn_backward(const void* x, const void* residual, const void* dy, void* dx, void* dresidual, int dtype,
+                    int64_t rows, int64_t C, const float* weight, const float* bias, const float* save_mean,
+                    const float* save_invstd, int relu, float* dweight, float* dbias, void* workspace,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,6 +18,7 @@ import torch
 class KernelTimer:
     def __init__(self):
         self.enabled = False
+        self.k5 = False            # also time the model-side K5 BatchNorm launches (bn.py)
         self.launches = 0          # every native kernel launch made through the package
         self._open = defaultdict(list)
 
@@ -28,6 +29,15 @@ class KernelTimer:
     def start(self, stream=None):
         self.launches += 1
         if not self.enabled:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream or torch.cuda.current_stream())
+        return ev
+
+    def start_k5(self, n_launches: int, stream=None):
+        """K5 calls launch ``n_launches`` kernels each; timed only when ``enabled and k5``."""
+        self.launches += n_launches
+        if not (self.enabled and self.k5):
             return None
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream or torch.cuda.current_stream())

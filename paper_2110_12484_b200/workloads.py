@@ -86,13 +86,21 @@ WORKLOADS = {
 }
 
 
-def build_model(w: Workload) -> nn.Module:
+def build_model(w: Workload, bn: str = "torch") -> nn.Module:
+    """The workload's model; ``bn="k5"`` routes its BatchNorm(+ReLU/+residual) through K5 (bn.py)."""
     if w.model in ("resnet18", "resnet50"):
         import torchvision
-        return getattr(torchvision.models, w.model)(num_classes=w.n_classes)
-    if w.model == "unet":
-        return UNet(w.sample_shape[0], 1)
-    raise ValueError(w.model)
+        m = getattr(torchvision.models, w.model)(num_classes=w.n_classes)
+    elif w.model == "unet":
+        m = UNet(w.sample_shape[0], 1)
+    else:
+        raise ValueError(w.model)
+    if bn == "k5":
+        from .bn import fuse_batchnorm
+        fuse_batchnorm(m)
+    elif bn != "torch":
+        raise ValueError(f"bn must be 'k5' or 'torch', got {bn!r}")
+    return m
 
 
 def synthetic_data(w: Workload, n: int, seed: int = 0, device="cpu", pinned: bool = False):

@@ -1,0 +1,52 @@
+"""K5 module rewrite on a CPU host: structure, names and the no-fallback rule (no kernel calls)."""
+import copy
+
+import pytest
+import torch
+import torchvision
+
+from paper_2110_12484_b200 import bn as K5
+from paper_2110_12484_b200.workloads import UNet
+
+
+@pytest.mark.parametrize("make", [lambda: torchvision.models.resnet18(num_classes=10),
+                                  lambda: torchvision.models.resnet50(num_classes=102), lambda: UNet(3, 1)])
+def test_fuse_keeps_parameters_buffers_and_order(make):
+    torch.manual_seed(0)
+    net = make()
+    ref = copy.deepcopy(net)
+    params = [id(p) for p in net.parameters()]
+    K5.fuse_batchnorm(net)
+    assert [id(p) for p in net.parameters()] == params            # same Parameter objects: ParameterSet-safe
+    assert list(net.state_dict()) == list(ref.state_dict())
+    n_bn = sum(isinstance(m, torch.nn.BatchNorm2d) for m in ref.modules())
+    mbn = [m for m in net.modules() if isinstance(m, K5.MicroBatchNorm2d)]
+    assert len(mbn) == n_bn
+    assert not any(type(m) is torch.nn.BatchNorm2d for m in net.modules())
+    assert not any(isinstance(m, torch.nn.ReLU) for m in net.modules()) or isinstance(net, torchvision.models.ResNet)
+    # eval-mode inference is torch's running-statistics normalisation: identical outputs on CPU
+    net.eval()
+    ref.eval()
+    x = torch.randn(2, 3, 32, 32)
+    with torch.no_grad():
+        torch.testing.assert_close(net(x), ref(x), rtol=1e-5, atol=1e-6)
+
+
+def test_fused_relu_counts_resnet50():
+    net = K5.fuse_batchnorm(torchvision.models.resnet50())
+    mbn = [m for m in net.modules() if isinstance(m, K5.MicroBatchNorm2d)]
+    # stem + 16 blocks x 3 fused with relu; 4 downsample BNs plain
+    assert sum(m.fuse_relu for m in mbn) == 1 + 16 * 3
+    assert sum(not m.fuse_relu for m in mbn) == 4
+
+
+def test_training_on_cpu_fails_loudly():
+    net = K5.fuse_batchnorm(torchvision.models.resnet18(num_classes=10)).train()
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        net(torch.randn(2, 3, 32, 32))
+
+
+def test_residual_requires_fused_relu():
+    m = K5.MicroBatchNorm2d(4)
+    with pytest.raises(ValueError):
+        K5.micro_batch_norm(torch.randn(2, 4), m.weight, m.bias, residual=torch.randn(2, 4))

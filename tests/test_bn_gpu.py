@@ -1,0 +1,198 @@
+"""K5 micro-batch BatchNorm (+ fused ReLU / residual) vs a float64 torch reference of the same op.
+
+Contract: fp32 activations — outputs, dx, dresidual, dweight, dbias, saved
+statistics and running statistics within rel-L2 1e-5 of float64 (the op's own
+fp32 rounding; measured ~1e-7); bf16 activations — no worse than torch's own
+bf16 channels-last BatchNorm against the same float64 reference (x 1.5 + a
+bf16 ulp of slack). Runs are bit-reproducible (fixed-order reductions). The
+module rewrite keeps every parameter / buffer / state-dict key and order.
+"""
+import copy
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2110_12484_b200 import bn as K5
+from tests.gpu_util import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref64(x, res, w, b, relu, dy, rm=None, rv=None, momentum=0.1, eps=1e-5):
+    """float64 reference: y = relu(bn(x) + res); grads via autograd; running stats torch-style."""
+    x64 = x.detach().double().requires_grad_(True)
+    r64 = None if res is None else res.detach().double().requires_grad_(True)
+    w64 = w.detach().double().requires_grad_(True)
+    b64 = b.detach().double().requires_grad_(True)
+    rm64 = None if rm is None else rm.double().clone()
+    rv64 = None if rv is None else rv.double().clone()
+    y = F.batch_norm(x64, rm64, rv64, w64, b64, True, momentum, eps)
+    if r64 is not None:
+        y = y + r64
+    if relu:
+        y = F.relu(y)
+    y.backward(dy.double())
+    dims = [0] + list(range(2, x.dim()))
+    mean = x64.detach().mean(dims)
+    var = x64.detach().var(dims, unbiased=False)
+    return dict(y=y.detach(), dx=x64.grad, dres=None if r64 is None else r64.grad, dw=w64.grad, db=b64.grad,
+                mean=mean, invstd=1.0 / torch.sqrt(var + eps), rm=rm64, rv=rv64)
+
+
+def _data(cuda, shape, dtype, seed, offset=3.0):
+    g = torch.Generator(device=cuda).manual_seed(seed)
+    C = shape[1]
+    x = (torch.randn(shape, device=cuda, generator=g) * 2.0 + offset).to(dtype)
+    res = torch.randn(shape, device=cuda, generator=g).to(dtype)
+    dy = torch.randn(shape, device=cuda, generator=g).to(dtype)
+    w = torch.randn(C, device=cuda, generator=g) * 0.5 + 1.0
+    b = torch.randn(C, device=cuda, generator=g) * 0.1
+    if x.dim() == 4:
+        x, res, dy = (t.contiguous(memory_format=torch.channels_last) for t in (x, res, dy))
+    return x, res, dy, w, b
+
+
+def _run(x, res, dy, w, b, relu, rm=None, rv=None):
+    xx = x.detach().clone().requires_grad_(True)
+    rr = None if res is None else res.detach().clone().requires_grad_(True)
+    ww = w.detach().clone().requires_grad_(True)
+    bb = b.detach().clone().requires_grad_(True)
+    y = K5.micro_batch_norm(xx, ww, bb, rm, rv, relu=relu, residual=rr)
+    y.backward(dy)
+    return dict(y=y.detach(), dx=xx.grad, dres=None if rr is None else rr.grad, dw=ww.grad, db=bb.grad)
+
+
+SHAPES = [(8, 64, 14, 14), (4, 256, 7, 9), (2, 2048, 3, 3), (16, 24, 5, 5), (3, 3, 11, 7), (2, 520, 2, 3),
+          (37, 40), (5, 2056, 1, 1)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("mode", ["plain", "relu", "relu_res"])
+def test_k5_fp32_vs_float64(cuda, shape, mode):
+    relu, use_res = mode != "plain", mode == "relu_res"
+    x, res, dy, w, b = _data(cuda, shape, torch.float32, seed=sum(shape) + len(mode))
+    res = res if use_res else None
+    C = shape[1]
+    rm0 = torch.randn(C, device=cuda) * 0.1
+    rv0 = torch.rand(C, device=cuda) + 0.5
+    rm, rv = rm0.clone(), rv0.clone()
+    got = _run(x, res, dy, w, b, relu, rm, rv)
+    want = _ref64(x, res, w, b, relu, dy, rm0, rv0)
+    for k in ("y", "dx", "dw", "db") + (("dres",) if use_res else ()):
+        err = rel_l2(got[k].double().cpu().numpy(), want[k].cpu().numpy())
+        assert err <= 1e-5, (k, err)
+    assert rel_l2(rm.double().cpu().numpy(), want["rm"].cpu().numpy()) <= 1e-6
+    assert rel_l2(rv.double().cpu().numpy(), want["rv"].cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("shape", [(32, 64, 28, 28), (16, 256, 14, 14), (32, 2048, 7, 7), (8, 128, 9, 13)])
+@pytest.mark.parametrize("mode", ["plain", "relu", "relu_res"])
+def test_k5_bf16_no_worse_than_torch(cuda, shape, mode):
+    relu, use_res = mode != "plain", mode == "relu_res"
+    x, res, dy, w, b = _data(cuda, shape, torch.bfloat16, seed=7)
+    res = res if use_res else None
+    got = _run(x, res, dy, w, b, relu)
+    want = _ref64(x, res, w, b, relu, dy)
+    # torch's own bf16 path of the same op
+    xt = x.detach().clone().requires_grad_(True)
+    rt = None if res is None else res.detach().clone().requires_grad_(True)
+    wt = w.detach().clone().requires_grad_(True)
+    bt = b.detach().clone().requires_grad_(True)
+    yt = F.batch_norm(xt, None, None, wt, bt, True, 0.1, 1e-5)
+    if rt is not None:
+        yt = yt + rt
+    if relu:
+        yt = F.relu(yt)
+    yt.backward(dy)
+    tgot = dict(y=yt.detach(), dx=xt.grad, dres=None if rt is None else rt.grad, dw=wt.grad, db=bt.grad)
+    for k in ("y", "dx", "dw", "db") + (("dres",) if use_res else ()):
+        ours = rel_l2(got[k].double().cpu().numpy(), want[k].cpu().numpy())
+        theirs = rel_l2(tgot[k].double().cpu().numpy(), want[k].cpu().numpy())
+        assert ours <= 1.5 * theirs + 4e-3, (k, ours, theirs)
+
+
+def test_k5_deterministic(cuda):
+    x, res, dy, w, b = _data(cuda, (16, 256, 14, 14), torch.bfloat16, seed=3)
+    a = _run(x, res, dy, w, b, True)
+    c = _run(x, res, dy, w, b, True)
+    for k in a:
+        assert torch.equal(a[k], c[k]), k
+
+
+def test_k5_unaligned_inputs_take_the_scalar_path(cuda):
+    # a storage offset of one float breaks 16-byte alignment: the V=1 kernels must give the same answer
+    x, _, dy, w, b = _data(cuda, (4, 64, 6, 6), torch.float32, seed=5)
+    base = torch.empty(x.numel() + 1, device=cuda)
+    base[1:].view(4, 6, 6, 64).copy_(x.permute(0, 2, 3, 1))
+    base.requires_grad_(True)
+    xu = base[1:].view(4, 6, 6, 64).permute(0, 3, 1, 2)          # channels-last strides, misaligned
+    assert xu.data_ptr() % 16 != 0 and xu.is_contiguous(memory_format=torch.channels_last)
+    y = K5.micro_batch_norm(xu, w, b, relu=True)
+    y.backward(dy)
+    dx = base.grad[1:].view(4, 6, 6, 64).permute(0, 3, 1, 2)
+    want = _ref64(x, None, w, b, True, dy)
+    assert rel_l2(dx.double().cpu().numpy(), want["dx"].cpu().numpy()) <= 1e-5
+    assert rel_l2(y.detach().double().cpu().numpy(), want["y"].cpu().numpy()) <= 1e-5
+
+
+def test_k5_nchw_input_is_converted(cuda):
+    x, res, dy, w, b = _data(cuda, (4, 32, 5, 5), torch.float32, seed=6)
+    got = _run(x.contiguous(), res.contiguous(), dy.contiguous(), w, b, True)
+    want = _ref64(x, res, w, b, True, dy)
+    for k in ("y", "dx", "dres", "dw", "db"):
+        assert rel_l2(got[k].double().cpu().numpy(), want[k].cpu().numpy()) <= 1e-5, k
+
+
+def test_k5_size_one_micro_batch_raises_like_torch(cuda):
+    m = K5.MicroBatchNorm2d(8).to(cuda).train()
+    with pytest.raises(ValueError, match="more than 1 value per channel"):
+        m(torch.randn(1, 8, 1, 1, device=cuda))
+    with pytest.raises(ValueError):
+        F.batch_norm(torch.randn(1, 8, 1, 1, device=cuda), None, None, training=True)
+
+
+def _models():
+    import torchvision
+    from paper_2110_12484_b200.workloads import UNet
+    torch.manual_seed(0)
+    return [("resnet18", torchvision.models.resnet18(num_classes=10), (6, 3, 32, 32)),
+            ("resnet50", torchvision.models.resnet50(num_classes=12), (4, 3, 64, 64)),
+            ("unet", UNet(3, 1), (2, 3, 32, 32))]
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2])
+def test_fused_model_no_worse_than_torch_model_fp32(cuda, idx):
+    """Whole models (fp32, TF32 off): fused-K5 vs torch BatchNorm, both against a float64 copy.
+
+    Small micro-batches make BN models ill-conditioned in fp32 (~1e-3 floor), so the
+    contract is relative to torch's own fp32 error on the same model and input.
+    """
+    name, net, shape = _models()[idx]
+    net = net.to(cuda).to(memory_format=torch.channels_last).train()
+    fused = K5.fuse_batchnorm(copy.deepcopy(net))
+    ref = copy.deepcopy(net).double()
+    assert list(fused.state_dict()) == list(net.state_dict())
+    assert [n for n, _ in fused.named_parameters()] == [n for n, _ in net.named_parameters()]
+    g = torch.Generator(device=cuda).manual_seed(1)
+    x = torch.randn(shape, device=cuda, generator=g).contiguous(memory_format=torch.channels_last)
+    res = {}
+    for key, m, xin in (("torch", net, x), ("ours", fused, x), ("f64", ref, x.double())):
+        out = m(xin)
+        (out ** 2).mean().backward()
+        res[key] = dict(out=out.detach().double().cpu().numpy(),
+                        grad=np.concatenate([p.grad.double().cpu().numpy().ravel() for p in m.parameters()]),
+                        bufs=np.concatenate([v.double().cpu().numpy().ravel() for k, v in m.state_dict().items()
+                                             if "running" in k]))
+    for k in ("out", "grad", "bufs"):
+        ours = rel_l2(res["ours"][k], res["f64"][k])
+        theirs = rel_l2(res["torch"][k], res["f64"][k])
+        assert ours <= max(1e-5, 1.5 * theirs), (name, k, ours, theirs)
+    nbt = [v for k, v in fused.state_dict().items() if k.endswith("num_batches_tracked")]
+    assert all(int(v) == 1 for v in nbt)
+    # eval mode: running statistics, same as torch
+    net.eval()
+    fused.eval()
+    with torch.no_grad():
+        assert rel_l2(fused(x).double().cpu().numpy(), net(x).double().cpu().numpy()) <= 1e-4

@@ -21,6 +21,7 @@ import torch
 import paper_2110_12484_b200 as mbs
 from oracle import mbs_oracle as O
 from oracle.hybrid import TorchGradFn
+from paper_2110_12484_b200 import bn as K5
 from paper_2110_12484_b200.workloads import UNet
 from tests.gpu_util import rel_l2
 
@@ -31,7 +32,7 @@ def _flat(d, names):
     return np.concatenate([np.asarray(d[n], np.float64).ravel() for n in names])
 
 
-def _case(cuda, net, loss_kind, x, y, n_b, n_mu, mode, opt):
+def _case(cuda, net, loss_kind, x, y, n_b, n_mu, mode, opt, fuse=False):
     net.train()
     ref = TorchGradFn(net, loss_kind)                               # float64 CPU copy
     ref32 = TorchGradFn(net, loss_kind, dtype=torch.float32)        # fp32 CPU: the noise floor
@@ -50,12 +51,15 @@ def _case(cuda, net, loss_kind, x, y, n_b, n_mu, mode, opt):
     plain = {n: p.grad.double().cpu().numpy() for n, p in pnet.named_parameters()}
     floor = rel_l2(_flat(plain, names), _flat(g64, names))
     dev_net = copy.deepcopy(net).to(cuda)
+    if fuse:                                  # the model's BatchNorm(+ReLU/+residual) on K5 instead of torch
+        K5.fuse_batchnorm(dev_net)
     params = mbs.ParameterSet(dev_net)
     total, st = mbs.mini_batch_gradient(dev_net, params, x.to(cuda), y.to(cuda), mbs.plan_split(n_b, n_mu), mode,
                                         loss_kind)
     got = {n: total[n].detach().double().cpu().numpy() for n in names}
     err = rel_l2(_flat(got, names), _flat(g64, names))
-    assert rel_l2(_flat(got, names), _flat(plain, names)) <= 1e-4
+    if not fuse:   # same kernels as the plain run: only cuDNN run-to-run noise between them
+        assert rel_l2(_flat(got, names), _flat(plain, names)) <= 1e-4
     assert err <= max(1e-5, 1.5 * floor), (err, floor, floor_cpu)
     assert st.loss == pytest.approx(st64["loss"], rel=1e-4)
     assert st.grad_norm == pytest.approx(st64["grad_norm"], rel=max(1e-5, 3 * floor))
@@ -85,21 +89,23 @@ def _case(cuda, net, loss_kind, x, y, n_b, n_mu, mode, opt):
     return err, floor, floor_cpu
 
 
+@pytest.mark.parametrize("fuse", [False, True], ids=["torch_bn", "k5_bn"])
 @pytest.mark.parametrize("mode", ["exact_weighted", "paper_faithful"])
-def test_resnet18_c1(cuda, mode):
+def test_resnet18_c1(cuda, mode, fuse):
     import torchvision
     torch.manual_seed(0)
     net = torchvision.models.resnet18(num_classes=10)
     g = torch.Generator().manual_seed(1)
     x = torch.randn(20, 3, 32, 32, generator=g)
     y = torch.randint(0, 10, (20,), generator=g)
-    _case(cuda, net, "cross_entropy", x, y, 20, 8, mode, "sgd")       # [8, 8, 4]: ragged tail
+    _case(cuda, net, "cross_entropy", x, y, 20, 8, mode, "sgd", fuse)  # [8, 8, 4]: ragged tail
 
 
-def test_unet_bce_dice(cuda):
+@pytest.mark.parametrize("fuse", [False, True], ids=["torch_bn", "k5_bn"])
+def test_unet_bce_dice(cuda, fuse):
     torch.manual_seed(0)
     net = UNet(3, 1)
     g = torch.Generator().manual_seed(2)
     x = torch.randn(6, 3, 32, 32, generator=g)
     y = (torch.rand(6, 1, 32, 32, generator=g) < 0.5).float()
-    _case(cuda, net, "bce_dice", x, y, 6, 4, "exact_weighted", "adam")  # [4, 2]
+    _case(cuda, net, "bce_dice", x, y, 6, 4, "exact_weighted", "adam", fuse)  # [4, 2]
