@@ -77,7 +77,8 @@ def _case(cuda, net, loss_kind, x, y, n_b, n_mu, mode, opt, fuse=False):
     wg = {n: params[n].detach().double().cpu().numpy() for n in names}
     werr = rel_l2(_flat(wg, names), _flat(w, names))
     if opt == "sgd":
-        assert rel_l2(_flat(wg, names), _flat(wp, names)) <= 1e-5
+        if not fuse:   # the plain run used the same model kernels
+            assert rel_l2(_flat(wg, names), _flat(wp, names)) <= 1e-5
         assert werr <= max(1e-5, 1.5 * wfloor), (werr, wfloor)
     else:
         # Adam's first step is lr*g/(|g|+eps): ill-conditioned for the elements whose gradient is within a
