@@ -27,13 +27,15 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "mbs_common.h"
+#include "mbs_tma.h"
 
 namespace mbs {
 
 constexpr int kBnThreads = 256;
-constexpr int kBnTargetCtas = 4 * 148;
 
 template <typename T, int V> struct BnIO;
 
@@ -124,6 +126,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_reduce(const T* __restrict__ 
     const int lane = tid % g.gv, rph = tid / g.gv;
     const int64_t c0 = ((int64_t)blockIdx.y * g.gv + lane) * V;
     const bool active = rph < g.rp && c0 < g.C;
+    cudaGridDependencySynchronize();  // PDL: x / dy come from the preceding kernel
     float s1[V], s2[V], k[V], sc[V], sh[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) { s1[i] = 0.f; s2[i] = 0.f; k[i] = 0.f; sc[i] = 0.f; sh[i] = 0.f; }
@@ -213,34 +216,56 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_reduce(const T* __restrict__ 
     }
 }
 
-// One warp per channel: merge the P CTA partials in fp64 (lane l takes partials
-// l, l+32, ... in order, then a fixed xor-tree) and derive the per-channel values.
-__device__ __forceinline__ void warp_merge(const float2* part, int P, int lane, double& a, double& q) {
+// TPC threads per channel (power of two, 32..256) merge the P CTA partials in fp64: thread j
+// sums partials j, j+TPC, ... in order, then a fixed xor tree within the warp and a fixed-order
+// sum over the channel's warps. Returns true on the thread that owns the channel's result.
+template <int TPC>
+__device__ __forceinline__ bool group_merge(const float2* part, int P, bool valid, double& a, double& q) {
+    __shared__ double red[2][kBnThreads / 32];
+    const int t = threadIdx.x % TPC;
     a = 0.0;
     q = 0.0;
-    for (int p = lane; p < P; p += 32) {
-        const float2 v = part[p];
-        a += (double)v.x;
-        q += (double)v.y;
+    if (valid) {
+#pragma unroll 4
+        for (int p = t; p < P; p += TPC) {
+            const float2 v = part[p];
+            a += (double)v.x;
+            q += (double)v.y;
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         a += __shfl_xor_sync(0xffffffffu, a, o);
         q += __shfl_xor_sync(0xffffffffu, q, o);
     }
+    if (TPC > 32) {
+        const int warp = threadIdx.x / 32;
+        if (threadIdx.x % 32 == 0) {
+            red[0][warp] = a;
+            red[1][warp] = q;
+        }
+        __syncthreads();
+        if (t == 0) {
+            a = 0.0;
+            q = 0.0;
+            for (int k = 0; k < TPC / 32; ++k) {
+                a += red[0][warp + k];
+                q += red[1][warp + k];
+            }
+        }
+    }
+    return valid && t == 0;
 }
 
-template <typename T>
-__global__ void k_bn_stats_finalize(const T* __restrict__ x, const float2* __restrict__ part, BnGeom g,
-                                    const float* __restrict__ w, const float* __restrict__ b, float* running_mean,
-                                    float* running_var, double momentum, double eps, float* __restrict__ save_mean,
-                                    float* __restrict__ save_invstd, float* __restrict__ coef) {
-    const int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    const int lane = threadIdx.x % 32;
-    if (c >= g.C) return;
+template <typename T, int TPC>
+__global__ void __launch_bounds__(kBnThreads) k_bn_stats_finalize(
+        const T* __restrict__ x, const float2* __restrict__ part, BnGeom g, const float* __restrict__ w,
+        const float* __restrict__ b, float* running_mean, float* running_var, double momentum, double eps,
+        float* __restrict__ save_mean, float* __restrict__ save_invstd, float* __restrict__ coef) {
+    const int64_t c = (int64_t)blockIdx.x * (kBnThreads / TPC) + threadIdx.x / TPC;
+    cudaGridDependencySynchronize();  // PDL: partials come from the statistics kernel
     double s1, s2;
-    warp_merge(part + c * g.P, g.P, lane, s1, s2);
-    if (lane == 0) {
+    if (group_merge<TPC>(part + c * g.P, g.P, c < g.C, s1, s2)) {
         const double m = (double)g.rows;
         const double K = (double)static_cast<float>(x[c]);
         const double dm = s1 / m;
@@ -261,26 +286,27 @@ __global__ void k_bn_stats_finalize(const T* __restrict__ x, const float2* __res
 }
 
 // backward finalize: dgamma = invstd * sum g(x-mean), dbeta = sum g; dx coefficients
-// dx = k1*g + A*(x-mean) + B with k1 = gamma*invstd, A = -k1*invstd*dgamma/M, B = -k1*dbeta/M.
-__global__ void k_bn_bwd_finalize(const float2* __restrict__ part, BnGeom g, const float* __restrict__ w,
-                                  const float* __restrict__ b, const float* __restrict__ mean,
-                                  const float* __restrict__ invstd, float* __restrict__ dweight,
-                                  float* __restrict__ dbias, float* __restrict__ coef) {
-    const int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    const int lane = threadIdx.x % 32;
-    if (c >= g.C) return;
+// dx = k1*g + A*(x-mean) + B with k1 = gamma*invstd, A = -k1*invstd*dgamma/M, B = -k1*dbeta/M
+// (stored: A, B, B - A*mean).
+template <int TPC>
+__global__ void __launch_bounds__(kBnThreads) k_bn_bwd_finalize(
+        const float2* __restrict__ part, BnGeom g, const float* __restrict__ w, const float* __restrict__ mean,
+        const float* __restrict__ invstd, float* __restrict__ dweight, float* __restrict__ dbias,
+        float* __restrict__ coef) {
+    const int64_t c = (int64_t)blockIdx.x * (kBnThreads / TPC) + threadIdx.x / TPC;
+    cudaGridDependencySynchronize();  // PDL: partials come from the backward reduce kernel
     double sg, sgx;
-    warp_merge(part + c * g.P, g.P, lane, sg, sgx);
-    if (lane == 0) {
+    if (group_merge<TPC>(part + c * g.P, g.P, c < g.C, sg, sgx)) {
         const double is = (double)invstd[c];
         const double dgam = sgx * is;
         if (dweight) dweight[c] = (float)dgam;
         if (dbias) dbias[c] = (float)sg;
         const double m = (double)g.rows;
         const double k1 = (w ? (double)w[c] : 1.0) * is;
-        coef[3 * c] = (float)k1;
-        coef[3 * c + 1] = (float)(-k1 * is * dgam / m);
-        coef[3 * c + 2] = (float)(-k1 * sg / m);
+        const double A = -k1 * is * dgam / m, B = -k1 * sg / m;
+        coef[3 * c] = (float)A;
+        coef[3 * c + 1] = (float)B;
+        coef[3 * c + 2] = (float)(B - A * (double)mean[c]);
     }
 }
 
@@ -290,6 +316,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_apply(const T* __restrict__ x
     const int tid = threadIdx.x;
     const int lane = tid % g.gv, rph = tid / g.gv;
     const int64_t c0 = ((int64_t)blockIdx.y * g.gv + lane) * V;
+    cudaGridDependencySynchronize();  // PDL: coef comes from the finalize kernel
     if (rph >= g.rp || c0 >= g.C) return;
     float sc[V], sh[V];
 #pragma unroll
@@ -333,7 +360,10 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_apply(const T* __restrict__ x
     }
 }
 
-// dx = k1*g + A*(x-mean) + B, g = dy * mask; with a residual, dres = g.
+// dx = k1*g + A*(x-mean) + B, g = dy * mask; with a residual, dres = g. k1 = gamma*invstd is
+// bit-identical to the forward scale (a float product; the fp64 product of two floats rounds to
+// the same value). bf16 activations use the folded dx = k1*g + (A*x + (B - A*mean)): the fp32
+// rounding of A*x (~6e-8 |A*mean|) is far below the bf16 output ulp, and it frees V registers.
 template <typename T, int V, bool RELU, bool RES>
 __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_elemt(const T* __restrict__ x, const T* __restrict__ dy,
                                                              const T* __restrict__ res, T* __restrict__ dx,
@@ -342,20 +372,19 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_elemt(const T* __restrict
                                                              const float* __restrict__ mean,
                                                              const float* __restrict__ invstd,
                                                              const float* __restrict__ coef, BnGeom g) {
+    constexpr bool kFold = sizeof(T) == 2;
     const int tid = threadIdx.x;
     const int lane = tid % g.gv, rph = tid / g.gv;
     const int64_t c0 = ((int64_t)blockIdx.y * g.gv + lane) * V;
+    cudaGridDependencySynchronize();  // PDL: coef comes from the finalize kernel
     if (rph >= g.rp || c0 >= g.C) return;
-    float k1[V], A[V], B[V], mu[V], sc[V], sh[V];
+    float A[V], B[V], mu[V], sc[V], sh[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-        k1[i] = coef[3 * (c0 + i)];
-        A[i] = coef[3 * (c0 + i) + 1];
-        B[i] = coef[3 * (c0 + i) + 2];
-        mu[i] = mean[c0 + i];
-        sc[i] = 0.f;
-        sh[i] = 0.f;
-        if (RELU) bn_affine(w, b, mean, invstd, c0 + i, sc[i], sh[i]);
+        A[i] = coef[3 * (c0 + i)];
+        B[i] = coef[3 * (c0 + i) + (kFold ? 2 : 1)];
+        mu[i] = kFold ? 0.f : mean[c0 + i];
+        bn_affine(w, b, mean, invstd, c0 + i, sc[i], sh[i]);
     }
     const int64_t r0 = (int64_t)blockIdx.x * g.chunk;
     const int64_t r1 = min(g.rows, r0 + g.chunk);
@@ -368,7 +397,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_elemt(const T* __restrict
         }
         if (RES) BnIO<T, V>::store(dres + o, dv);
 #pragma unroll
-        for (int i = 0; i < V; ++i) xv[i] = fmaf(k1[i], dv[i], fmaf(A[i], xv[i] - mu[i], B[i]));
+        for (int i = 0; i < V; ++i) xv[i] = fmaf(sc[i], dv[i], fmaf(A[i], kFold ? xv[i] : xv[i] - mu[i], B[i]));
         BnIO<T, V>::store(dx + o, xv);
     };
     for (; r + (U - 1) * g.rp < r1; r += U * g.rp) {
@@ -392,6 +421,168 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_elemt(const T* __restrict
         body(xv, dv, rv, o);
     }
 }
+
+// ---------------------------------------------------------------------------------------------
+// Bulk-async (TMA) streaming path — used whenever one CTA covers every channel (C <= 256 vectors)
+// and the tensors are 16-byte aligned, i.e. for every BatchNorm of the benchmark models.
+//
+// A CTA owns a contiguous run of rows, which in NHWC is one contiguous byte range per tensor.
+// One elected thread keeps kTmaStages tiles (tile_rows rows of every input tensor) in flight
+// with cp.async.bulk into a smem ring, completion counted in bytes on the stage's mbarrier; the
+// 256 threads consume a landed stage (thread = channel vector x row phase, 16-byte conflict-free
+// smem reads), then the stage is refilled. So memory-level parallelism comes from the copy engine
+// (up to 4 x 24 KB per CTA, 2 CTAs per SM), not from per-thread registers. Outputs leave with
+// coalesced 16-byte stores. KIND: 0 statistics, 1 backward reduce, 2 apply, 3 backward elemt.
+// ---------------------------------------------------------------------------------------------
+constexpr int kTmaStages = 4;        // ring depth (A/B on B200: deeper rings of 6-12 stages were slower)
+constexpr int kTmaTileBytes = 8192;  // per input tensor per stage
+constexpr int kMaxTmaCtas = 4 * 148; // bounds the TMA path's partials (workspace)
+
+template <int KIND, bool RES>
+__host__ __device__ constexpr int tma_inputs() {
+    return 1 + ((KIND == 1 || KIND == 3) ? 1 : 0) + (RES ? 1 : 0);
+}
+
+
+template <typename T, int V, int KIND, bool RELU, bool RES>
+__global__ void __launch_bounds__(kBnThreads, 2) k_bn_tma(
+        const T* __restrict__ x, const T* __restrict__ dy, const T* __restrict__ res, T* __restrict__ out,
+        T* __restrict__ dres, const float* __restrict__ w, const float* __restrict__ b,
+        const float* __restrict__ mean, const float* __restrict__ invstd, const float* __restrict__ coef,
+        float2* __restrict__ part, BnGeom g, int tile_rows) {
+    constexpr int NIN = tma_inputs<KIND, RES>();
+    constexpr bool kFold = sizeof(T) == 2;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full[kTmaStages];
+    const int tid = threadIdx.x;
+    const int lane = tid % g.gv, rph = tid / g.gv;
+    const int64_t c0 = (int64_t)lane * V;
+    const bool active = rph < g.rp;
+    const int64_t r0 = (int64_t)blockIdx.x * g.chunk;
+    const int64_t r1 = min(g.rows, r0 + g.chunk);
+    const int n_tiles = (int)((r1 - r0 + tile_rows - 1) / tile_rows);
+
+    cudaGridDependencySynchronize();  // PDL: inputs / coefficients come from the preceding kernel
+
+    auto issue = [&](int i) {
+        const int64_t rs = r0 + (int64_t)i * tile_rows;
+        const uint32_t bytes = (uint32_t)(min((int64_t)tile_rows, r1 - rs) * g.C * (int64_t)sizeof(T));
+        const int st = i % kTmaStages;
+        unsigned char* slot = smem + (size_t)st * NIN * kTmaTileBytes;
+        mbar_expect_tx(&full[st], bytes * NIN);
+        bulk_load(slot, x + rs * g.C, bytes, &full[st]);
+        int k = 1;
+        if (KIND == 1 || KIND == 3) bulk_load(slot + (k++) * kTmaTileBytes, dy + rs * g.C, bytes, &full[st]);
+        if (RES) bulk_load(slot + k * kTmaTileBytes, res + rs * g.C, bytes, &full[st]);
+    };
+    if (tid == 0) {
+        for (int st = 0; st < kTmaStages; ++st) mbar_init(&full[st], 1);
+        mbar_init_fence();
+        for (int i = 0; i < min(kTmaStages, n_tiles); ++i) issue(i);
+    }
+
+    // per-channel state in registers
+    float s1[V], s2[V], kk[V], sc[V], sh[V], A[V], B[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        s1[i] = s2[i] = kk[i] = sc[i] = sh[i] = A[i] = B[i] = 0.f;
+    }
+    if (active) {
+        if (KIND == 0) BnIO<T, V>::load(x + c0, kk);  // shift K = x[0, c]
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            if (KIND == 1) kk[i] = mean[c0 + i];
+            if (KIND == 3 && !kFold) kk[i] = mean[c0 + i];
+            if ((KIND == 1 && RELU) || KIND == 3) bn_affine(w, b, mean, invstd, c0 + i, sc[i], sh[i]);
+            if (KIND == 2) {
+                sc[i] = coef[2 * (c0 + i)];
+                sh[i] = coef[2 * (c0 + i) + 1];
+            }
+            if (KIND == 3) {
+                A[i] = coef[3 * (c0 + i)];
+                B[i] = coef[3 * (c0 + i) + (kFold ? 2 : 1)];
+            }
+        }
+    }
+    __syncthreads();  // barriers initialised
+
+    for (int i = 0; i < n_tiles; ++i) {
+        const int st = i % kTmaStages;
+        const int64_t rs = r0 + (int64_t)i * tile_rows;
+        const int nr = (int)min((int64_t)tile_rows, r1 - rs);
+        mbar_wait(&full[st], (uint32_t)((i / kTmaStages) & 1));
+        const T* xs = reinterpret_cast<const T*>(smem + (size_t)st * NIN * kTmaTileBytes);
+        const T* ds = reinterpret_cast<const T*>(smem + ((size_t)st * NIN + 1) * kTmaTileBytes);
+        const T* rsm = reinterpret_cast<const T*>(smem + ((size_t)st * NIN + NIN - 1) * kTmaTileBytes);
+        if (active) {
+#pragma unroll 2
+            for (int j = rph; j < nr; j += g.rp) {
+                const int64_t o = (int64_t)j * g.C + c0;
+                float xv[V], dv[V], rv[V];
+                BnIO<T, V>::load(xs + o, xv);
+                if (KIND == 1 || KIND == 3) BnIO<T, V>::load(ds + o, dv);
+                if (RES) BnIO<T, V>::load(rsm + o, rv);
+                if ((KIND == 1 || KIND == 3) && RELU) {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) dv[e] = relu_mask<T, V, RES>(xv[e], sc[e], sh[e], rv[e], dv[e]);
+                }
+                if (KIND == 0) {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        const float d = xv[e] - kk[e];
+                        s1[e] += d;
+                        s2[e] = fmaf(d, d, s2[e]);
+                    }
+                } else if (KIND == 1) {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        s1[e] += dv[e];
+                        s2[e] = fmaf(dv[e], xv[e] - kk[e], s2[e]);
+                    }
+                } else if (KIND == 2) {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        const float z = fmaf(xv[e], sc[e], sh[e]) + (RES ? rv[e] : 0.f);
+                        xv[e] = RELU ? relu_nan(z) : z;
+                    }
+                    BnIO<T, V>::store(out + (rs + j) * g.C + c0, xv);
+                } else {
+                    if (RES) BnIO<T, V>::store(dres + (rs + j) * g.C + c0, dv);
+#pragma unroll
+                    for (int e = 0; e < V; ++e)
+                        xv[e] = fmaf(sc[e], dv[e], fmaf(A[e], kFold ? xv[e] : xv[e] - kk[e], B[e]));
+                    BnIO<T, V>::store(out + (rs + j) * g.C + c0, xv);
+                }
+            }
+        }
+        __syncthreads();  // stage st consumed by every thread
+        if (tid == 0 && i + kTmaStages < n_tiles) issue(i + kTmaStages);
+    }
+
+    if (KIND == 0 || KIND == 1) {
+        // CTA reduction over the row phases (fixed order) into this CTA's partial; the ring is free now
+        float* red0 = reinterpret_cast<float*>(smem);
+        float* red1 = red0 + kBnThreads * V;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            red0[e * kBnThreads + tid] = s1[e];
+            red1[e * kBnThreads + tid] = s2[e];
+        }
+        __syncthreads();
+        const int gc = g.gv * V;
+        for (int j = tid; j < gc; j += kBnThreads) {
+            const int ln = j / V, e = j % V;
+            float a = 0.f, q = 0.f;
+            for (int p = 0; p < g.rp; ++p) {
+                a += red0[e * kBnThreads + p * g.gv + ln];
+                q += red1[e * kBnThreads + p * g.gv + ln];
+            }
+            part[(int64_t)j * g.P + blockIdx.x] = make_float2(a, q);
+        }
+    }
+}
+
+constexpr int kMaxReduceCtas = 2048;  // bounds the partials (workspace) per BatchNorm call
 
 static BnGeom bn_geom(int64_t rows, int64_t C, int V, int64_t min_rows_per_thread, int target_ctas) {
     BnGeom g;
@@ -420,6 +611,146 @@ static int bn_vec(int dtype, int64_t C, const void* const* ptrs, int n) {
 
 static int64_t bn_groups(const BnGeom& g, int V) { return (g.C / V + g.gv - 1) / g.gv; }
 
+static int sm_count() {
+    static int n = 0;
+    if (n <= 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
+// One full wave of the kernel: resident CTAs per SM (registers / smem limited) x SMs.
+template <typename K>
+static int wave_ctas(K kernel) {
+    static std::mutex mu;
+    static std::map<const void*, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find((const void*)kernel);
+    if (it != cache.end()) return it->second;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBnThreads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const int n = per_sm * sm_count();
+    cache[(const void*)kernel] = n;
+    return n;
+}
+
+// Every K5 kernel is launched with programmatic stream serialization (PDL): its launch and
+// prologue overlap the previous kernel's tail; griddepcontrol.wait (cudaGridDependencySynchronize)
+// at the top of each kernel orders its reads after the producer's writes.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kBnThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+static int tpc_for(int P) {
+    int t = 32;
+    while (t < 256 && 2 * t < P) t *= 2;
+    return t;
+}
+
+template <typename T, int V, int MODE, bool RELU, bool RES>
+static cudaError_t launch_reduce(const T* X, const T* DY, const T* R, const float* w, const float* b,
+                                 const float* mean, const float* invstd, float2* part, BnGeom& g, cudaStream_t s) {
+    auto k = k_bn_reduce<T, V, MODE, RELU, RES>;
+    g = bn_geom(g.rows, g.C, V, 32, std::min(wave_ctas(k), kMaxReduceCtas));
+    return launch_pdl(k, dim3(g.P, (unsigned)bn_groups(g, V)), s, X, DY, R, w, b, mean, invstd, part, g);
+}
+
+template <typename T, int TPC>
+static cudaError_t launch_stats_finalize(const T* X, const float2* part, const BnGeom& g, const float* w,
+                                         const float* b, float* rm, float* rv, double momentum, double eps,
+                                         float* smean, float* sinv, float* coef, cudaStream_t s) {
+    const unsigned grid = (unsigned)((g.C + kBnThreads / TPC - 1) / (kBnThreads / TPC));
+    return launch_pdl(k_bn_stats_finalize<T, TPC>, dim3(grid), s, X, part, g, w, b, rm, rv, momentum, eps, smean,
+                      sinv, coef);
+}
+
+template <int TPC>
+static cudaError_t launch_bwd_finalize(const float2* part, const BnGeom& g, const float* w, const float* mean,
+                                       const float* invstd, float* dw, float* db, float* coef, cudaStream_t s) {
+    const unsigned grid = (unsigned)((g.C + kBnThreads / TPC - 1) / (kBnThreads / TPC));
+    return launch_pdl(k_bn_bwd_finalize<TPC>, dim3(grid), s, part, g, w, mean, invstd, dw, db, coef);
+}
+
+template <typename T, int V, bool RELU, bool RES>
+static cudaError_t launch_apply(const T* X, const T* R, T* Y, const float* coef, int64_t rows, int64_t C,
+                                cudaStream_t s) {
+    auto k = k_bn_apply<T, V, RELU, RES>;
+    BnGeom g = bn_geom(rows, C, V, 4, wave_ctas(k));
+    return launch_pdl(k, dim3(g.P, (unsigned)bn_groups(g, V)), s, X, R, Y, coef, g);
+}
+
+template <typename T, int V, bool RELU, bool RES>
+static cudaError_t launch_elemt(const T* X, const T* DY, const T* R, T* DX, T* DR, const float* w, const float* b,
+                                const float* mean, const float* invstd, const float* coef, int64_t rows, int64_t C,
+                                cudaStream_t s) {
+    auto k = k_bn_bwd_elemt<T, V, RELU, RES>;
+    BnGeom g = bn_geom(rows, C, V, 4, wave_ctas(k));
+    return launch_pdl(k, dim3(g.P, (unsigned)bn_groups(g, V)), s, X, DY, R, DX, DR, w, b, mean, invstd, coef, g);
+}
+
+static int tma_tile_rows(const BnGeom& g, int elem_bytes) {
+    int64_t rows = kTmaTileBytes / (g.C * elem_bytes);
+    rows = rows / g.rp * g.rp;
+    return (int)std::max<int64_t>(rows, g.rp);
+}
+
+// Geometry of the TMA path: one channel group, CTAs = min(resident CTAs, tiles), each CTA a
+// contiguous run of whole tiles.
+template <typename T, int V, int KIND, bool RELU, bool RES>
+static cudaError_t launch_tma(const T* X, const T* DY, const T* R, T* OUT, T* DR, const float* w, const float* b,
+                              const float* mean, const float* invstd, const float* coef, float2* part,
+                              BnGeom& g, cudaStream_t s) {
+  if constexpr (V == 1) {
+    return cudaErrorInvalidValue;  // never taken: tma_ok() requires 16-byte vectors
+  } else {
+    auto k = k_bn_tma<T, V, KIND, RELU, RES>;
+    constexpr int NIN = tma_inputs<KIND, RES>();
+    const size_t smem = (size_t)kTmaStages * NIN * kTmaTileBytes;
+    static int per_sm = 0;  // one static per template instance
+    if (per_sm == 0) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBnThreads, smem) != cudaSuccess || per_sm < 1)
+            per_sm = 1;
+    }
+    g = bn_geom(g.rows, g.C, V, 1, 1);  // gv / rp for one group
+    const int tr = tma_tile_rows(g, (int)sizeof(T));
+    const int64_t tiles = (g.rows + tr - 1) / tr;
+    int64_t ctas = std::min<int64_t>(std::min(per_sm * sm_count(), kMaxTmaCtas), tiles);
+    ctas = std::max<int64_t>(ctas, 1);
+    const int64_t tiles_per_cta = (tiles + ctas - 1) / ctas;
+    g.chunk = tiles_per_cta * tr;
+    g.P = (int)((g.rows + g.chunk - 1) / g.chunk);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g.P);
+    cfg.blockDim = dim3(kBnThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, X, DY, R, OUT, DR, w, b, mean, invstd, coef, part, g, tr);
+  }
+}
+
+static bool tma_ok(int64_t C, int V) { return V > 1 && C / V <= kBnThreads; }
+
 template <typename T, int V>
 static int bn_forward_t(const void* x, const void* res, void* y, int64_t rows, int64_t C, const float* w,
                         const float* b, float* rm, float* rv, double momentum, double eps, int relu, float* smean,
@@ -427,23 +758,34 @@ static int bn_forward_t(const void* x, const void* res, void* y, int64_t rows, i
     const T* X = static_cast<const T*>(x);
     const T* R = static_cast<const T*>(res);
     T* Y = static_cast<T*>(y);
-    BnGeom gr = bn_geom(rows, C, V, 32, kBnTargetCtas);
     float* coef = static_cast<float*>(ws);
-    float2* part = reinterpret_cast<float2*>(coef + 2 * ((C + 3) / 4 * 4));
-    dim3 grid(gr.P, (unsigned)bn_groups(gr, V));
-    k_bn_reduce<T, V, 0, false, false><<<grid, kBnThreads, 0, s>>>(X, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                                                   nullptr, part, gr);
-    MBS_CK_LAUNCH("k_bn_reduce(stats)");
-    k_bn_stats_finalize<T><<<(unsigned)((C + 7) / 8), 256, 0, s>>>(X, part, gr, w, b, rm, rv, momentum, eps, smean,
-                                                                   sinv, coef);
-    MBS_CK_LAUNCH("k_bn_stats_finalize");
-    BnGeom ga = bn_geom(rows, C, V, 8, 8 * 148);
-    dim3 ga_grid(ga.P, (unsigned)bn_groups(ga, V));
-    if (relu && res) k_bn_apply<T, V, true, true><<<ga_grid, kBnThreads, 0, s>>>(X, R, Y, coef, ga);
-    else if (relu) k_bn_apply<T, V, true, false><<<ga_grid, kBnThreads, 0, s>>>(X, R, Y, coef, ga);
-    else if (res) k_bn_apply<T, V, false, true><<<ga_grid, kBnThreads, 0, s>>>(X, R, Y, coef, ga);
-    else k_bn_apply<T, V, false, false><<<ga_grid, kBnThreads, 0, s>>>(X, R, Y, coef, ga);
-    MBS_CK_LAUNCH("k_bn_apply");
+    float2* part = reinterpret_cast<float2*>(coef + 3 * ((C + 3) / 4 * 4));
+    BnGeom g;
+    g.rows = rows;
+    g.C = C;
+    const bool tma = tma_ok(C, V);
+    // statistics: the register-pipelined kernel (ncu A/B on B200: 40 us vs 48 us through the bulk-async
+    // ring for a 205 MB single read-only stream); apply / backward use the ring.
+    MBS_CK((launch_reduce<T, V, 0, false, false>(X, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, part, g,
+                                                  s)));
+    const int tpc = tpc_for(g.P);
+    cudaError_t e;
+    if (tpc == 32) e = launch_stats_finalize<T, 32>(X, part, g, w, b, rm, rv, momentum, eps, smean, sinv, coef, s);
+    else if (tpc == 64) e = launch_stats_finalize<T, 64>(X, part, g, w, b, rm, rv, momentum, eps, smean, sinv, coef, s);
+    else if (tpc == 128) e = launch_stats_finalize<T, 128>(X, part, g, w, b, rm, rv, momentum, eps, smean, sinv, coef, s);
+    else e = launch_stats_finalize<T, 256>(X, part, g, w, b, rm, rv, momentum, eps, smean, sinv, coef, s);
+    MBS_CK(e);
+    BnGeom ga = g;
+    if (tma && relu && res)
+        e = launch_tma<T, V, 2, true, true>(X, nullptr, R, Y, nullptr, w, b, smean, sinv, coef, nullptr, ga, s);
+    else if (tma && relu)
+        e = launch_tma<T, V, 2, true, false>(X, nullptr, R, Y, nullptr, w, b, smean, sinv, coef, nullptr, ga, s);
+    else if (tma)
+        e = launch_tma<T, V, 2, false, false>(X, nullptr, R, Y, nullptr, w, b, smean, sinv, coef, nullptr, ga, s);
+    else if (relu && res) e = launch_apply<T, V, true, true>(X, R, Y, coef, rows, C, s);
+    else if (relu) e = launch_apply<T, V, true, false>(X, R, Y, coef, rows, C, s);
+    else e = launch_apply<T, V, false, false>(X, R, Y, coef, rows, C, s);
+    MBS_CK(e);
     return MBS_OK;
 }
 
@@ -454,32 +796,42 @@ static int bn_backward_t(const void* x, const void* res, const void* dy, void* d
     const T* X = static_cast<const T*>(x);
     const T* R = static_cast<const T*>(res);
     const T* DY = static_cast<const T*>(dy);
-    BnGeom gr = bn_geom(rows, C, V, 32, kBnTargetCtas);
     float* coef = static_cast<float*>(ws);
     float2* part = reinterpret_cast<float2*>(coef + 3 * ((C + 3) / 4 * 4));
-    dim3 grid(gr.P, (unsigned)bn_groups(gr, V));
-    if (relu && res)
-        k_bn_reduce<T, V, 1, true, true><<<grid, kBnThreads, 0, s>>>(X, DY, R, w, b, smean, sinv, part, gr);
-    else if (relu)
-        k_bn_reduce<T, V, 1, true, false><<<grid, kBnThreads, 0, s>>>(X, DY, R, w, b, smean, sinv, part, gr);
-    else
-        k_bn_reduce<T, V, 1, false, false><<<grid, kBnThreads, 0, s>>>(X, DY, R, w, b, smean, sinv, part, gr);
-    MBS_CK_LAUNCH("k_bn_reduce(backward)");
-    k_bn_bwd_finalize<<<(unsigned)((C + 7) / 8), 256, 0, s>>>(part, gr, w, b, smean, sinv, dw, db, coef);
-    MBS_CK_LAUNCH("k_bn_bwd_finalize");
-    BnGeom ge = bn_geom(rows, C, V, 8, 8 * 148);
-    dim3 ge_grid(ge.P, (unsigned)bn_groups(ge, V));
+    BnGeom g;
+    g.rows = rows;
+    g.C = C;
+    cudaError_t e;
+    const bool tma = tma_ok(C, V);
+    if (tma && relu && res)
+        e = launch_tma<T, V, 1, true, true>(X, DY, R, nullptr, nullptr, w, b, smean, sinv, nullptr, part, g, s);
+    else if (tma && relu)
+        e = launch_tma<T, V, 1, true, false>(X, DY, R, nullptr, nullptr, w, b, smean, sinv, nullptr, part, g, s);
+    else if (tma)
+        e = launch_tma<T, V, 1, false, false>(X, DY, R, nullptr, nullptr, w, b, smean, sinv, nullptr, part, g, s);
+    else if (relu && res) e = launch_reduce<T, V, 1, true, true>(X, DY, R, w, b, smean, sinv, part, g, s);
+    else if (relu) e = launch_reduce<T, V, 1, true, false>(X, DY, R, w, b, smean, sinv, part, g, s);
+    else e = launch_reduce<T, V, 1, false, false>(X, DY, R, w, b, smean, sinv, part, g, s);
+    MBS_CK(e);
+    const int tpc = tpc_for(g.P);
+    if (tpc == 32) e = launch_bwd_finalize<32>(part, g, w, smean, sinv, dw, db, coef, s);
+    else if (tpc == 64) e = launch_bwd_finalize<64>(part, g, w, smean, sinv, dw, db, coef, s);
+    else if (tpc == 128) e = launch_bwd_finalize<128>(part, g, w, smean, sinv, dw, db, coef, s);
+    else e = launch_bwd_finalize<256>(part, g, w, smean, sinv, dw, db, coef, s);
+    MBS_CK(e);
     T* DX = static_cast<T*>(dx);
     T* DR = static_cast<T*>(dres);
-    if (relu && res)
-        k_bn_bwd_elemt<T, V, true, true><<<ge_grid, kBnThreads, 0, s>>>(X, DY, R, DX, DR, w, b, smean, sinv, coef, ge);
-    else if (relu)
-        k_bn_bwd_elemt<T, V, true, false><<<ge_grid, kBnThreads, 0, s>>>(X, DY, R, DX, DR, w, b, smean, sinv, coef,
-                                                                         ge);
-    else
-        k_bn_bwd_elemt<T, V, false, false><<<ge_grid, kBnThreads, 0, s>>>(X, DY, R, DX, DR, w, b, smean, sinv, coef,
-                                                                          ge);
-    MBS_CK_LAUNCH("k_bn_bwd_elemt");
+    BnGeom ge = g;
+    if (tma && relu && res)
+        e = launch_tma<T, V, 3, true, true>(X, DY, R, DX, DR, w, b, smean, sinv, coef, nullptr, ge, s);
+    else if (tma && relu)
+        e = launch_tma<T, V, 3, true, false>(X, DY, R, DX, DR, w, b, smean, sinv, coef, nullptr, ge, s);
+    else if (tma)
+        e = launch_tma<T, V, 3, false, false>(X, DY, R, DX, DR, w, b, smean, sinv, coef, nullptr, ge, s);
+    else if (relu && res) e = launch_elemt<T, V, true, true>(X, DY, R, DX, DR, w, b, smean, sinv, coef, rows, C, s);
+    else if (relu) e = launch_elemt<T, V, true, false>(X, DY, R, DX, DR, w, b, smean, sinv, coef, rows, C, s);
+    else e = launch_elemt<T, V, false, false>(X, DY, R, DX, DR, w, b, smean, sinv, coef, rows, C, s);
+    MBS_CK(e);
     return MBS_OK;
 }
 
@@ -495,8 +847,13 @@ int mbs_bn_workspace_bytes(int64_t rows, int64_t C, int dtype, int64_t* bytes) {
     int64_t worst = 0;
     for (int V : {1, dtype == MBS_BF16 ? 8 : 4}) {
         if (C % V) continue;
-        BnGeom g = bn_geom(rows, C, V, 32, kBnTargetCtas);
-        worst = std::max<int64_t>(worst, (int64_t)g.P * C * 8);
+        BnGeom g = bn_geom(rows, C, V, 32, kMaxReduceCtas);  // generic path: P never exceeds this bound
+        int64_t P = g.P;
+        if (tma_ok(C, V)) {                                     // TMA path: min(resident CTAs, tiles)
+            const int tr = tma_tile_rows(g, dtype == MBS_BF16 ? 2 : 4);
+            P = std::max<int64_t>(P, std::min<int64_t>(kMaxTmaCtas, (rows + tr - 1) / tr));
+        }
+        worst = std::max<int64_t>(worst, P * C * 8);
     }
     *bytes = 3 * 4 * ((C + 3) / 4 * 4) + worst;
     return MBS_OK;
