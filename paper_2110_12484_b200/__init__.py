@@ -4,10 +4,12 @@ Drop-in for the reference package ``mbstream``'s hot path (engine / optim /
 tensor / memory / streaming APIs, same names and exception types), running
 on hand-written sm_100a kernels behind the C-ABI ``libmbs_native.so``
 (``include/mbs.h``): K1 fused normalise+accumulate+grad-norm, K2 staging,
-K3 fused optimizer step, plus the pinned H2D micro-batch streamer.
+K3 fused optimizer step, plus the pinned H2D micro-batch streamer; K5 runs the
+model's micro-batch BatchNorm (+ReLU/+skip add) when a model is passed through
+``bn.fuse_batchnorm``.
 """
 
-from . import _native
+from . import _native, bn
 from .engine import (NORMALIZATION_MODES, EpochStats, GradientAccumulator, MicroBatchPlan, MiniBatchStats,
                      accumulate, make_streamer, mini_batch_gradient, normalization_factor, normalize_loss,
                      plan_split, train_epoch, train_mini_batch)

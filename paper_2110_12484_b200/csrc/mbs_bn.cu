@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_reduce(const T* __restrict__ 
         }
         const int64_t r0 = (int64_t)blockIdx.x * g.chunk;
         const int64_t r1 = min(g.rows, r0 + g.chunk);
-        constexpr int U = 4;
+        constexpr int U = MODE == 0 ? 8 : 4;  // statistics: one stream, more loads in flight per thread
         int64_t r = r0 + rph;
         for (; r + (U - 1) * g.rp < r1; r += U * g.rp) {
             float xv[U][V], dv[U][V], rv[U][V];
@@ -665,7 +665,7 @@ template <typename T, int V, int MODE, bool RELU, bool RES>
 static cudaError_t launch_reduce(const T* X, const T* DY, const T* R, const float* w, const float* b,
                                  const float* mean, const float* invstd, float2* part, BnGeom& g, cudaStream_t s) {
     auto k = k_bn_reduce<T, V, MODE, RELU, RES>;
-    g = bn_geom(g.rows, g.C, V, 32, std::min(wave_ctas(k), kMaxReduceCtas));
+    g = bn_geom(g.rows, g.C, V, MODE == 0 ? 16 : 32, std::min(wave_ctas(k), kMaxReduceCtas));
     return launch_pdl(k, dim3(g.P, (unsigned)bn_groups(g, V)), s, X, DY, R, w, b, mean, invstd, part, g);
 }
 
@@ -847,7 +847,7 @@ int mbs_bn_workspace_bytes(int64_t rows, int64_t C, int dtype, int64_t* bytes) {
     int64_t worst = 0;
     for (int V : {1, dtype == MBS_BF16 ? 8 : 4}) {
         if (C % V) continue;
-        BnGeom g = bn_geom(rows, C, V, 32, kMaxReduceCtas);  // generic path: P never exceeds this bound
+        BnGeom g = bn_geom(rows, C, V, 16, kMaxReduceCtas);  // generic path (statistics: 16 rows/thread): P bound
         int64_t P = g.P;
         if (tma_ok(C, V)) {                                     // TMA path: min(resident CTAs, tiles)
             const int tr = tma_tile_rows(g, dtype == MBS_BF16 ? 2 : 4);

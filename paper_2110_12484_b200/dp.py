@@ -34,8 +34,8 @@ from contextlib import nullcontext
 import numpy as np
 import torch
 
-from .engine import (GradientAccumulator, MicroBatchPlan, MiniBatchStats, normalization_factor, plan_split,
-                     _as_tensor, _micro_source, make_streamer)
+from .engine import (GradientAccumulator, MicroBatchPlan, MiniBatchStats, _as_tensor, _micro_source, make_streamer,
+                     normalization_factor, plan_split, weight_cast_cache)
 from .losses import compute_loss
 from .optim import apply_update
 from .tensor import ParameterSet
@@ -387,6 +387,18 @@ class DataParallelMBS:
         losses, factors, weights = [], [], []
         works = []
         plist = acc._plist
+        cast_cache = weight_cast_cache(autocast_dtype)    # one weight cast per mini-batch (engine.py)
+        cast_cache.__enter__()
+        try:
+            self._micro_loop(model, plan, block, source, normalization, loss_kind, acc, ctx, loss_from_logits,
+                             dice_smoothing, n_local, losses, factors, weights, works, plist)
+        finally:
+            cast_cache.__exit__(None, None, None)
+        return self._exchange_and_step(model, plan, block, optimizer_state, acc, n_local, losses, factors, weights,
+                                       works, bn, lr_for_step)
+
+    def _micro_loop(self, model, plan, block, source, normalization, loss_kind, acc, ctx, loss_from_logits,
+                    dice_smoothing, n_local, losses, factors, weights, works, plist):
         for j in range(n_local):
             xk, yk = next(source)
             k = block[0] + j
@@ -445,6 +457,9 @@ class DataParallelMBS:
                 from .errors import AccumulatorOverflowError
                 raise AccumulatorOverflowError("a parameter received no gradient on the last micro-batch")
             launch_ready()
+
+    def _exchange_and_step(self, model, plan, block, optimizer_state, acc, n_local, losses, factors, weights,
+                           works, bn, lr_for_step):
         for wk in works:
             wk.wait()
         if n_local == 0:

@@ -497,6 +497,29 @@ def _run_micro_loop(model, acc, plan, source, normalization, loss_kind, loss_fro
     """The micro loop; K1 records (raw loss, factor, size_k) per micro for the stats."""
     outputs = []
     ctx = torch.autocast("cuda", dtype=autocast_dtype) if autocast_dtype is not None else nullcontext()
+    with weight_cast_cache(autocast_dtype):
+        return _micro_loop_body(model, acc, plan, source, normalization, loss_kind, loss_from_logits,
+                                dice_smoothing, normalize_via, ctx, keep_outputs, outputs)
+
+
+def weight_cast_cache(autocast_dtype):
+    """Keep torch's autocast weight-cast cache alive across the micro-batches of ONE mini-batch.
+
+    The weights are constant until the optimizer step that follows the last
+    micro-batch, so each fp32 master weight needs its low-precision copy once
+    per mini-batch, not once per micro-batch (ResNet-50: 54 casts and 142 MB
+    of traffic per micro saved). torch clears the cache when the OUTERMOST
+    autocast region exits; an outer region with autocast DISABLED keeps the
+    nesting count up without changing how forward or backward run. The cache
+    is dropped when this region exits, i.e. before the optimizer step.
+    """
+    if autocast_dtype is None:
+        return nullcontext()
+    return torch.autocast("cuda", dtype=autocast_dtype, enabled=False)
+
+
+def _micro_loop_body(model, acc, plan, source, normalization, loss_kind, loss_from_logits, dice_smoothing,
+                     normalize_via, ctx, keep_outputs, outputs):
     k = -1
     for k, (xk, yk) in enumerate(source):
         if k >= plan.n_s_mu:
