@@ -158,8 +158,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=16, help="samples per CPU-reference step")
-    ap.add_argument("--model-bn", default="k5", choices=["k5", "torch"],
-                    help="the model's BatchNorm(+ReLU/+residual): K5 sm_100a kernels or stock torch")
+    ap.add_argument("--model-ops", default="native", choices=["native", "torch"],
+                    help="the model's BatchNorm(+ReLU/+skip add) and max-pool: K5/K6 sm_100a kernels or stock torch")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -205,7 +205,7 @@ def main():
     torch.backends.cudnn.benchmark = True
     torch.manual_seed(1234 + rank)
 
-    model = build_model(w, bn=args.model_bn).to(dev).to(memory_format=torch.channels_last)
+    model = build_model(w, ops=args.model_ops).to(dev).to(memory_format=torch.channels_last)
     params = mbs.ParameterSet(model)
     staging = Staging(dtype=torch.bfloat16, channels_last=True)
     autocast = torch.bfloat16
@@ -300,7 +300,7 @@ def main():
     launches_value = TIMER.launches
     # K5 (model BatchNorm) bandwidth: one more HBM-resident mini-batch with its launches timed (not in `value`)
     k5stats = {}
-    if args.model_bn == "k5":
+    if args.model_ops == "native":
         TIMER.reset()
         TIMER.enabled = TIMER.k5 = True
         epoch(False, 1, 2000, warm_mini)
@@ -322,9 +322,9 @@ def main():
     streamer.close()
 
     # --- no-stream baseline: plain torch training at batch = micro, data resident ---
-    nos = no_stream_baseline(w, dev, n_mu, args.steps, args.warmup, ws, bn=args.model_bn)
-    nos_torch = (no_stream_baseline(w, dev, n_mu, args.steps, args.warmup, ws, bn="torch")
-                 if args.model_bn != "torch" else None)
+    nos = no_stream_baseline(w, dev, n_mu, args.steps, args.warmup, ws, ops=args.model_ops)
+    nos_torch = (no_stream_baseline(w, dev, n_mu, args.steps, args.warmup, ws, ops="torch")
+                 if args.model_ops != "torch" else None)
 
     # the reference's overhead report (streaming.py:130-149) on MEASURED schedules: the MBS step as
     # run (copy per micro from the streamer's events, compute per micro from the timed step) vs the
@@ -360,6 +360,20 @@ def main():
                               "(acc = s*g); P = %d" % params.layout.n_params,
                 "other_kernels": {k: {"gbs": v["gbs"], "avg_us": v["avg_ms"] * 1e3, "launches": v["launches"]}
                                   for k, v in kstats.items() if k != "k1_accumulate"}}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            _pk = json.load(f)
+        tf_peak, tf_kind = float(_pk["bf16_tflops_sustained"]), "measured sustained bf16"
+    except Exception:
+        tf_peak, tf_kind = 1407.5, "fallback (SURVEY §8d sustained bf16)"
+    from paper_2110_12484_b200.workloads import gflop_per_sample
+    gfs = gflop_per_sample(w, dev)
+    model_flops = {"bound": "tensor", "gflop_per_sample": gfs, "unit": "TFLOP/s",
+                   "achieved": value * gfs / 1e3, "achieved_e2e": e2e * gfs / 1e3, "peak": tf_peak,
+                   "peak_kind": tf_kind, "frac": value / ws * gfs / 1e3 / tf_peak,
+                   "frac_e2e": e2e / ws * gfs / 1e3 / tf_peak, "peak_is": "per GPU (frac uses value / n_gpus)",
+                   "how": "end-to-end samples/s x algorithmic fwd+bwd FLOP per sample (FlopCounterMode: the "
+                          "model's convolutions/matmuls), against the bf16 dense peak"}
     roofline_k5 = None
     if k5stats:
         kb = sum(v["bytes_per_launch"] * v["launches"] for v in k5stats.values())
@@ -381,8 +395,9 @@ def main():
                        "n_micro": plan.n_s_mu, "global_batch": n_b * ws, "parallelism": f"dp{ws}",
                        "normalization": w.normalization, "optimizer": w.optimizer,
                        "model_precision": "bf16 autocast on cuDNN/cuBLAS, fp32 master weights; MBS path fp32",
-                       "model_bn": ("BatchNorm(+ReLU/+residual) on K5 sm_100a kernels (bn.py), micro-batch "
-                                    "statistics" if args.model_bn == "k5" else "stock torch BatchNorm"),
+                       "model_ops": ("BatchNorm(+ReLU/+skip add) on K5 and max-pool on K6 sm_100a kernels "
+                                     "(bn.py, pool.py), micro-batch statistics" if args.model_ops == "native"
+                                     else "stock torch BatchNorm / max-pool"),
                        "input": "uint8 NCHW staged to bf16 NHWC by K2",
                        "l2": ("inputs > L2: every mini-batch is %.0f MB of uint8" % (x_dev[:n_b].numel() / 1e6)) +
                              ", none reused within the timed region",
@@ -394,7 +409,7 @@ def main():
                     "d2h_bytes_per_step": 8 * (4 + 2 * plan.n_s_mu), "ms_per_step": ms_host / args.steps},
             "h2d_overlap_pct": overlap, "h2d_gbs": h2d_gbs, "accum_gbs": k1.get("gbs"),
             "no_stream": nos, "stream_vs_no_stream": value / nos["value"] if nos else None, "overhead": overhead,
-            "no_stream_torch_bn": nos_torch, "roofline_k5": roofline_k5,
+            "no_stream_torch_ops": nos_torch, "roofline_k5": roofline_k5, "model_flops": model_flops,
             "e2e_vs_no_stream": e2e / nos["value"] if nos else None,
             "roofline": roofline, "gpu_launches": launches_value, "gpu_launches_e2e": launches_e2e,
             "clocks": clocks.summary(), "final_loss": losses[-1] if losses else None}
@@ -412,14 +427,14 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def no_stream_baseline(w, dev, batch, steps, warmup, ws, bn="torch"):
+def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch"):
     """The paper's 'w/o MBS' run: plain torch training, batch = micro-batch, data resident in HBM.
 
-    ``bn`` selects the same model definition as the MBS run (K5 or stock torch BatchNorm)."""
+    ``ops`` selects the same model definition as the MBS run (native K5/K6 or stock torch ops)."""
     from paper_2110_12484_b200.losses import compute_loss
     from paper_2110_12484_b200.workloads import build_model, synthetic_data
     torch.manual_seed(0)
-    model = build_model(w, bn=bn).to(dev).to(memory_format=torch.channels_last)
+    model = build_model(w, ops=ops).to(dev).to(memory_format=torch.channels_last)
     if w.optimizer == "sgd":
         opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9, weight_decay=5e-4, fused=True)
     else:
@@ -450,7 +465,7 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, bn="torch"):
     ms = e0.elapsed_time(e1)
     del model, opt
     return {"value": batch * n * ws / (ms / 1e3), "unit": "samples/s", "batch": batch,
-            "steps": n, "model_bn": bn,
+            "steps": n, "model_ops": ops,
             "how": "torch fwd/bwd + fused torch.optim step per batch, bf16 autocast, data in HBM"}
 
 

@@ -248,6 +248,19 @@ int mbs_bn_backward(const void* x, const void* residual, const void* dy, void* d
                     const float* save_invstd, int relu, float* dweight, float* dbias, void* workspace,
                     void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Max-pool (K6) — the model's MaxPool2d in every micro-batch forward/backward,
+ * channels-last. x [N,H,W,C], y / idx / dy [N,Ho,Wo,C] with Ho = (H+2p-k)/s+1;
+ * idx holds the window-relative argmax (kh*k + kw, one byte). torch semantics
+ * (first maximum wins, NaN propagates, padding never wins); the backward sums
+ * the gradients of an input element in ascending window order in fp32, so both
+ * directions are bit-identical to torch's max_pool2d. dilation 1, floor mode.
+ * ------------------------------------------------------------------------- */
+int mbs_maxpool_forward(const void* x, void* y, uint8_t* idx, int dtype, int64_t N, int64_t H, int64_t W, int64_t C,
+                        int k, int s, int p, void* stream);
+int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype, int64_t N, int64_t H, int64_t W,
+                         int64_t C, int k, int s, int p, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,98 @@
+"""Channels-last max-pool on sm_100a (K6, ``csrc/mbs_pool.cu``) for the model's MaxPool2d.
+
+torch's NHWC max-pool keeps an int64 index per output element; on B200 it was
+8.5 % of the ResNet-50 micro-batch step (``profiles/r01_c2_v3_launches.md``) and
+~10 % of the U-Net@384 step. K6 keeps a one-byte window-relative argmax and a
+gather backward; forward and backward are bit-identical to ``F.max_pool2d``
+(first maximum wins, NaN propagates, ascending-order fp32 gradient sums).
+
+``swap_maxpool(model)`` turns every supported ``nn.MaxPool2d`` (square kernel,
+stride and padding, dilation 1, floor mode, no returned indices) into a
+:class:`MicroMaxPool2d` in place; parameters and state dicts are untouched
+(max-pool has none). CUDA bf16/fp32 activations always run K6 (a missing
+``libmbs_native.so`` raises); CPU tensors use torch (eval / oracle runs).
+"""
+
+from __future__ import annotations
+
+import torch
+from torch import nn
+
+from . import _native
+from .prof import TIMER
+
+_DTYPES = {torch.bfloat16: _native.BF16, torch.float32: _native.F32}
+
+
+def _square(v):
+    if isinstance(v, (tuple, list)):
+        return v[0] if len(v) == 2 and v[0] == v[1] else None
+    return v
+
+
+class _MaxPoolFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, k, s, p):
+        code = _DTYPES.get(x.dtype)
+        if code is None:
+            raise ValueError(f"K6 max-pool supports bfloat16 / float32, got {x.dtype}")
+        x = x.contiguous(memory_format=torch.channels_last)
+        n, c, h, w = x.shape
+        ho, wo = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+        y = torch.empty((n, c, ho, wo), dtype=x.dtype, device=x.device, memory_format=torch.channels_last)
+        idx = torch.empty((n, ho, wo, c), dtype=torch.uint8, device=x.device)
+        stream = torch.cuda.current_stream(x.device)
+        TIMER.launches += 1
+        _native.check(_native.lib().mbs_maxpool_forward(x.data_ptr(), y.data_ptr(), idx.data_ptr(), code, n, h, w, c,
+                                                        k, s, p, stream.cuda_stream), "mbs_maxpool_forward")
+        ctx.save_for_backward(idx)
+        ctx.geom = (n, c, h, w, k, s, p, code)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        (idx,) = ctx.saved_tensors
+        n, c, h, w, k, s, p, code = ctx.geom
+        dy = dy.contiguous(memory_format=torch.channels_last)
+        if _DTYPES.get(dy.dtype) != code:
+            dy = dy.to(idx.device).to({_native.BF16: torch.bfloat16, _native.F32: torch.float32}[code])
+        dx = torch.empty((n, c, h, w), dtype=dy.dtype, device=dy.device, memory_format=torch.channels_last)
+        stream = torch.cuda.current_stream(dy.device)
+        TIMER.launches += 1
+        _native.check(_native.lib().mbs_maxpool_backward(dy.data_ptr(), idx.data_ptr(), dx.data_ptr(), code, n, h, w,
+                                                         c, k, s, p, stream.cuda_stream), "mbs_maxpool_backward")
+        return dx, None, None, None
+
+
+def max_pool2d(x, kernel_size: int, stride: int | None = None, padding: int = 0):
+    """Functional K6 max-pool (square window, dilation 1, floor mode)."""
+    return _MaxPoolFn.apply(x, int(kernel_size), int(stride or kernel_size), int(padding))
+
+
+class MicroMaxPool2d(nn.MaxPool2d):
+    """``nn.MaxPool2d`` whose CUDA forward/backward run K6 (bit-identical to torch)."""
+
+    def forward(self, x):
+        if not x.is_cuda or x.dim() != 4:
+            return super().forward(x)
+        return _MaxPoolFn.apply(x, self._k, self._s, self._p)
+
+
+def supported(m: nn.MaxPool2d) -> bool:
+    k, s, p, d = _square(m.kernel_size), _square(m.stride or m.kernel_size), _square(m.padding), _square(m.dilation)
+    return (None not in (k, s, p, d) and d == 1 and not m.ceil_mode and not m.return_indices and k * k <= 255
+            and 0 <= 2 * p <= k)
+
+
+def swap_maxpool(model: nn.Module) -> nn.Module:
+    """Route every supported ``nn.MaxPool2d`` of ``model`` through K6 (in place; returns the model)."""
+    for m in model.modules():
+        if type(m) is nn.MaxPool2d and supported(m):
+            m.__class__ = MicroMaxPool2d
+            m._k = int(_square(m.kernel_size))
+            m._s = int(_square(m.stride or m.kernel_size))
+            m._p = int(_square(m.padding))
+    return model
+
+
+__all__ = ["MicroMaxPool2d", "max_pool2d", "swap_maxpool", "supported"]

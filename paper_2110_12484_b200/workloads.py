@@ -86,8 +86,9 @@ WORKLOADS = {
 }
 
 
-def build_model(w: Workload, bn: str = "torch") -> nn.Module:
-    """The workload's model; ``bn="k5"`` routes its BatchNorm(+ReLU/+residual) through K5 (bn.py)."""
+def build_model(w: Workload, ops: str = "torch") -> nn.Module:
+    """The workload's model. ``ops="native"`` runs its BatchNorm(+ReLU/+skip add) on K5 (bn.py) and its
+    max-pools on K6 (pool.py); ``"torch"`` is the stock module. Parameters are identical either way."""
     if w.model in ("resnet18", "resnet50"):
         import torchvision
         m = getattr(torchvision.models, w.model)(num_classes=w.n_classes)
@@ -95,12 +96,27 @@ def build_model(w: Workload, bn: str = "torch") -> nn.Module:
         m = UNet(w.sample_shape[0], 1)
     else:
         raise ValueError(w.model)
-    if bn == "k5":
+    if ops == "native":
         from .bn import fuse_batchnorm
+        from .pool import swap_maxpool
         fuse_batchnorm(m)
-    elif bn != "torch":
-        raise ValueError(f"bn must be 'k5' or 'torch', got {bn!r}")
+        swap_maxpool(m)
+    elif ops != "torch":
+        raise ValueError(f"ops must be 'native' or 'torch', got {ops!r}")
     return m
+
+
+def gflop_per_sample(w: Workload, device) -> float:
+    """Algorithmic fwd+bwd GFLOP per sample of the workload's model (torch FlopCounterMode over the
+    convolutions / matmuls of a 2-sample fp32 step; ResNet-50@224 24.29, U-Net@384 649.75)."""
+    from torch.utils.flop_counter import FlopCounterMode
+    m = build_model(w).to(device).to(memory_format=torch.channels_last).train()
+    x = torch.randn((2,) + w.sample_shape, device=device).contiguous(memory_format=torch.channels_last)
+    with FlopCounterMode(display=False) as fc:
+        m(x).float().sum().backward()
+    total = fc.get_total_flops()
+    del m, x
+    return total / 2 / 1e9
 
 
 def synthetic_data(w: Workload, n: int, seed: int = 0, device="cpu", pinned: bool = False):

@@ -50,3 +50,25 @@ def test_residual_requires_fused_relu():
     m = K5.MicroBatchNorm2d(4)
     with pytest.raises(ValueError):
         K5.micro_batch_norm(torch.randn(2, 4), m.weight, m.bias, residual=torch.randn(2, 4))
+
+
+def test_swap_maxpool_supported_configs():
+    from paper_2110_12484_b200 import pool as K6
+    m = torch.nn.Sequential(torch.nn.MaxPool2d(3, 2, 1), torch.nn.MaxPool2d(2), torch.nn.MaxPool2d(3, 2, 1, ceil_mode=True),
+                            torch.nn.MaxPool2d(3, 2, 1, dilation=2), torch.nn.MaxPool2d((3, 2)))
+    K6.swap_maxpool(m)
+    kinds = [type(x).__name__ for x in m]
+    assert kinds == ["MicroMaxPool2d", "MicroMaxPool2d", "MaxPool2d", "MaxPool2d", "MaxPool2d"]
+    x = torch.randn(2, 4, 9, 9)
+    torch.testing.assert_close(m[0](x), torch.nn.functional.max_pool2d(x, 3, 2, 1))   # CPU: torch path
+
+
+def test_build_model_native_ops():
+    from paper_2110_12484_b200.workloads import WORKLOADS, build_model
+    from paper_2110_12484_b200 import pool as K6
+    a = build_model(WORKLOADS["c2"], ops="native")
+    b = build_model(WORKLOADS["c2"], ops="torch")
+    assert list(a.state_dict()) == list(b.state_dict())
+    assert isinstance(a.maxpool, K6.MicroMaxPool2d)
+    with pytest.raises(ValueError):
+        build_model(WORKLOADS["c2"], ops="k5")

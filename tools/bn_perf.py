@@ -8,6 +8,7 @@ import torchvision
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2110_12484_b200 import bn as K5  # noqa: E402
+from paper_2110_12484_b200 import pool as K6  # noqa: E402
 from paper_2110_12484_b200.workloads import UNet  # noqa: E402
 
 
@@ -61,10 +62,11 @@ def models():
             m = make().to(dev).to(memory_format=torch.channels_last).train()
             if fused:
                 K5.fuse_batchnorm(m)
+                K6.swap_maxpool(m)
             x = torch.randn(shape, device=dev).to(memory_format=torch.channels_last)
             y = tgt(shape[0])
             ms, one = step_ms(m, x, y, lf)
-            print(f"{name} {'K5 fused' if fused else 'torch BN'}: {ms:.2f} ms/step "
+            print(f"{name} {'K5+K6 native' if fused else 'torch ops'}: {ms:.2f} ms/step "
                   f"({shape[0] / ms * 1000:.0f} samples/s)", flush=True)
             top_kernels(one)
             del m, x, y

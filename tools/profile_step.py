@@ -17,12 +17,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--host", action="store_true")
 ap.add_argument("--warmup", type=int, default=2)
-ap.add_argument("--model-bn", default="k5", choices=["k5", "torch"])
+ap.add_argument("--model-ops", default="native", choices=["native", "torch"])
 args = ap.parse_args()
 w = WORKLOADS[args.config]
 dev = torch.device("cuda:0")
 torch.backends.cudnn.benchmark = True
-model = build_model(w, bn=args.model_bn).to(dev).to(memory_format=torch.channels_last)
+model = build_model(w, ops=args.model_ops).to(dev).to(memory_format=torch.channels_last)
 params = mbs.ParameterSet(model)
 plan = mbs.plan_split(w.mini, w.micro)
 x, y = synthetic_data(w, w.mini, device="cpu" if args.host else dev)
