@@ -256,10 +256,16 @@ int mbs_bn_backward(const void* x, const void* residual, const void* dy, void* d
  * the gradients of an input element in ascending window order in fp32, so both
  * directions are bit-identical to torch's max_pool2d. dilation 1, floor mode.
  * ------------------------------------------------------------------------- */
+/* stash (nullable): also write x into channel columns [stash_c0, stash_c0+C) of a channels-last
+ * tensor with stash_C channels (the U-Net skip lands in its concat buffer); needs k == s, p == 0,
+ * k | H, k | W (every input element read exactly once). */
 int mbs_maxpool_forward(const void* x, void* y, uint8_t* idx, int dtype, int64_t N, int64_t H, int64_t W, int64_t C,
-                        int k, int s, int p, void* stream);
+                        int k, int s, int p, void* stash, int64_t stash_C, int64_t stash_c0, void* stream);
+/* addend (nullable): dx += addend[..., add_c0:add_c0+C] (channels-last, add_C channels), summed in
+ * fp32 before dx's single rounding (the skip-connection gradient, fused). */
 int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype, int64_t N, int64_t H, int64_t W,
-                         int64_t C, int k, int s, int p, void* stream);
+                         int64_t C, int k, int s, int p, const void* addend, int64_t add_C, int64_t add_c0,
+                         void* stream);
 
 #ifdef __cplusplus
 }

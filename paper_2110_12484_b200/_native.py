@@ -79,9 +79,9 @@ _SIGS = {
     "mbs_bn_backward": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "mbs_maxpool_forward": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64, c_int,
-                                    c_int, c_int, c_void_p]),
+                                    c_int, c_int, c_void_p, c_int64, c_int64, c_void_p]),
     "mbs_maxpool_backward": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64,
-                                     c_int, c_int, c_int, c_void_p]),
+                                     c_int, c_int, c_int, c_void_p, c_int64, c_int64, c_void_p]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -98,9 +98,14 @@ __device__ __forceinline__ void load_idx(const uint8_t* p, uint8_t (&v)[V]) {
     }
 }
 
+// Optional side copy ("stash"): with non-overlapping windows covering the input (k == s, p == 0,
+// k | H, k | W) every input element is read exactly once, so the kernel also writes it into channel
+// columns [sc0, sc0 + C) of a wider channels-last tensor with row stride sC — the U-Net skip
+// connection lands in its concat buffer without a separate torch.cat pass.
 template <typename T, int V>
 __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restrict__ x, T* __restrict__ y,
-                                                              uint8_t* __restrict__ idx, PoolGeom g) {
+                                                              uint8_t* __restrict__ idx, PoolGeom g,
+                                                              T* __restrict__ stash, int64_t sC, int64_t sc0) {
     cudaGridDependencySynchronize();
     const int64_t cv = g.C / V;
     const int64_t total = g.N * g.Ho * g.Wo * cv;
@@ -126,7 +131,9 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restric
                 const int64_t iw = w0 + kw;
                 if (iw < 0 || iw >= g.W) continue;
                 float v[V];
-                PoolIO<T, V>::load(x + ((n * g.H + ih) * g.W + iw) * g.C + c0, v);
+                const int64_t pix = (n * g.H + ih) * g.W + iw;
+                PoolIO<T, V>::load(x + pix * g.C + c0, v);
+                if (stash) PoolIO<T, V>::store(stash + pix * sC + sc0 + c0, v);
                 const uint8_t pos = (uint8_t)(kh * g.k + kw);
 #pragma unroll
                 for (int i = 0; i < V; ++i) {
@@ -143,10 +150,14 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restric
     }
 }
 
+// Optional addend: dx += add[pixel, ac0 + c] (row stride aC) in fp32 before the single rounding —
+// the gradient that reached the same tensor through the U-Net skip connection, fused instead of
+// autograd's separate add pass.
 template <typename T, int V>
 __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restrict__ dy,
                                                               const uint8_t* __restrict__ idx, T* __restrict__ dx,
-                                                              PoolGeom g) {
+                                                              PoolGeom g, const T* __restrict__ add, int64_t aC,
+                                                              int64_t ac0) {
     cudaGridDependencySynchronize();
     const int64_t cv = g.C / V;
     const int64_t total = g.N * g.H * g.W * cv;
@@ -186,7 +197,14 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
                     if (a[i] == pos) acc[i] += d[i];
             }
         }
-        PoolIO<T, V>::store(dx + ((n * g.H + ih) * g.W + iw) * g.C + c0, acc);
+        const int64_t pix = (n * g.H + ih) * g.W + iw;
+        if (add) {
+            float a2[V];
+            PoolIO<T, V>::load(add + pix * aC + ac0 + c0, a2);
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] += a2[i];
+        }
+        PoolIO<T, V>::store(dx + pix * g.C + c0, acc);
     }
 }
 
@@ -239,50 +257,68 @@ using namespace mbs;
 extern "C" {
 
 int mbs_maxpool_forward(const void* x, void* y, uint8_t* idx, int dtype, int64_t N, int64_t H, int64_t W, int64_t C,
-                        int k, int s, int p, void* stream) {
+                        int k, int s, int p, void* stash, int64_t stash_C, int64_t stash_c0, void* stream) {
     if (!x || !y || !idx) return invalid("mbs_maxpool_forward: null pointer");
     PoolGeom g;
     int st = pool_check(dtype, N, H, W, C, k, s, p, &g);
     if (st) return st;
+    if (stash && !(k == s && p == 0 && H % k == 0 && W % k == 0))
+        return invalid("mbs_maxpool_forward: a stash needs non-overlapping windows tiling the input (k == s, p == 0)");
+    if (stash && (stash_c0 < 0 || stash_c0 + C > stash_C)) return invalid("mbs_maxpool_forward: stash columns");
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     const int64_t outs = g.N * g.Ho * g.Wo;
+    const int es = dtype == MBS_BF16 ? 2 : 4;
+    const bool stash_vec = !stash || (!(reinterpret_cast<uintptr_t>(stash) & 15) && (stash_C * es) % 16 == 0 &&
+                                      (stash_c0 * es) % 16 == 0);
     cudaError_t e;
     if (dtype == MBS_BF16) {
         using T = __nv_bfloat16;
-        if (C % 8 == 0 && aligned16(x, y, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7))
-            e = pool_launch(k_maxpool_fwd<T, 8>, outs * (C / 8), cs, (const T*)x, (T*)y, idx, g);
+        if (C % 8 == 0 && aligned16(x, y, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7) && stash_vec)
+            e = pool_launch(k_maxpool_fwd<T, 8>, outs * (C / 8), cs, (const T*)x, (T*)y, idx, g, (T*)stash, stash_C,
+                            stash_c0);
         else
-            e = pool_launch(k_maxpool_fwd<T, 1>, outs * C, cs, (const T*)x, (T*)y, idx, g);
+            e = pool_launch(k_maxpool_fwd<T, 1>, outs * C, cs, (const T*)x, (T*)y, idx, g, (T*)stash, stash_C, stash_c0);
     } else {
-        if (C % 4 == 0 && aligned16(x, y, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 3))
-            e = pool_launch(k_maxpool_fwd<float, 4>, outs * (C / 4), cs, (const float*)x, (float*)y, idx, g);
+        if (C % 4 == 0 && aligned16(x, y, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 3) && stash_vec)
+            e = pool_launch(k_maxpool_fwd<float, 4>, outs * (C / 4), cs, (const float*)x, (float*)y, idx, g,
+                            (float*)stash, stash_C, stash_c0);
         else
-            e = pool_launch(k_maxpool_fwd<float, 1>, outs * C, cs, (const float*)x, (float*)y, idx, g);
+            e = pool_launch(k_maxpool_fwd<float, 1>, outs * C, cs, (const float*)x, (float*)y, idx, g, (float*)stash,
+                            stash_C, stash_c0);
     }
     MBS_CK(e);
     return MBS_OK;
 }
 
 int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype, int64_t N, int64_t H, int64_t W,
-                         int64_t C, int k, int s, int p, void* stream) {
+                         int64_t C, int k, int s, int p, const void* addend, int64_t add_C, int64_t add_c0,
+                         void* stream) {
     if (!dy || !idx || !dx) return invalid("mbs_maxpool_backward: null pointer");
     PoolGeom g;
     int st = pool_check(dtype, N, H, W, C, k, s, p, &g);
     if (st) return st;
+    if (addend && (add_c0 < 0 || add_c0 + C > add_C)) return invalid("mbs_maxpool_backward: addend columns");
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     const int64_t ins = g.N * g.H * g.W;
+    const int es = dtype == MBS_BF16 ? 2 : 4;
+    const bool add_vec = !addend || (!(reinterpret_cast<uintptr_t>(addend) & 15) && (add_C * es) % 16 == 0 &&
+                                     (add_c0 * es) % 16 == 0);
     cudaError_t e;
     if (dtype == MBS_BF16) {
         using T = __nv_bfloat16;
-        if (C % 8 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7))
-            e = pool_launch(k_maxpool_bwd<T, 8>, ins * (C / 8), cs, (const T*)dy, idx, (T*)dx, g);
+        if (C % 8 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7) && add_vec)
+            e = pool_launch(k_maxpool_bwd<T, 8>, ins * (C / 8), cs, (const T*)dy, idx, (T*)dx, g, (const T*)addend,
+                            add_C, add_c0);
         else
-            e = pool_launch(k_maxpool_bwd<T, 1>, ins * C, cs, (const T*)dy, idx, (T*)dx, g);
+            e = pool_launch(k_maxpool_bwd<T, 1>, ins * C, cs, (const T*)dy, idx, (T*)dx, g, (const T*)addend, add_C,
+                            add_c0);
     } else {
-        if (C % 4 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 3))
-            e = pool_launch(k_maxpool_bwd<float, 4>, ins * (C / 4), cs, (const float*)dy, idx, (float*)dx, g);
+        if (C % 4 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 3) && add_vec)
+            e = pool_launch(k_maxpool_bwd<float, 4>, ins * (C / 4), cs, (const float*)dy, idx, (float*)dx, g,
+                            (const float*)addend, add_C, add_c0);
         else
-            e = pool_launch(k_maxpool_bwd<float, 1>, ins * C, cs, (const float*)dy, idx, (float*)dx, g);
+            e = pool_launch(k_maxpool_bwd<float, 1>, ins * C, cs, (const float*)dy, idx, (float*)dx, g,
+                            (const float*)addend, add_C, add_c0);
     }
     MBS_CK(e);
     return MBS_OK;

@@ -44,7 +44,7 @@ class _MaxPoolFn(torch.autograd.Function):
         stream = torch.cuda.current_stream(x.device)
         TIMER.launches += 1
         _native.check(_native.lib().mbs_maxpool_forward(x.data_ptr(), y.data_ptr(), idx.data_ptr(), code, n, h, w, c,
-                                                        k, s, p, stream.cuda_stream), "mbs_maxpool_forward")
+                                                        k, s, p, None, 0, 0, stream.cuda_stream), "mbs_maxpool_forward")
         ctx.save_for_backward(idx)
         ctx.geom = (n, c, h, w, k, s, p, code)
         return y
@@ -60,8 +60,79 @@ class _MaxPoolFn(torch.autograd.Function):
         stream = torch.cuda.current_stream(dy.device)
         TIMER.launches += 1
         _native.check(_native.lib().mbs_maxpool_backward(dy.data_ptr(), idx.data_ptr(), dx.data_ptr(), code, n, h, w,
-                                                         c, k, s, p, stream.cuda_stream), "mbs_maxpool_backward")
+                                                         c, k, s, p, None, 0, 0, stream.cuda_stream),
+                      "mbs_maxpool_backward")
         return dx, None, None, None
+
+
+class _PoolStashFn(torch.autograd.Function):
+    """(maxpool_k(s), buf): buf is a channels-last concat buffer with s in channels [0, C_s) and
+    ``c_extra`` channels left for the decoder's upsampled tensor (written later by ``join_skip``).
+
+    Backward fuses the skip-connection gradient: ds = maxpool_bwd(d_pooled) + d_buf[:, :C_s]."""
+
+    @staticmethod
+    def forward(ctx, s, k, c_extra):
+        code = _DTYPES.get(s.dtype)
+        if code is None:
+            raise ValueError(f"K6 max-pool supports bfloat16 / float32, got {s.dtype}")
+        s = s.contiguous(memory_format=torch.channels_last)
+        n, c, h, w = s.shape
+        y = torch.empty((n, c, h // k, w // k), dtype=s.dtype, device=s.device, memory_format=torch.channels_last)
+        idx = torch.empty((n, h // k, w // k, c), dtype=torch.uint8, device=s.device)
+        buf = torch.empty((n, c + c_extra, h, w), dtype=s.dtype, device=s.device, memory_format=torch.channels_last)
+        stream = torch.cuda.current_stream(s.device)
+        TIMER.launches += 1
+        _native.check(_native.lib().mbs_maxpool_forward(s.data_ptr(), y.data_ptr(), idx.data_ptr(), code, n, h, w, c,
+                                                        k, k, 0, buf.data_ptr(), c + c_extra, 0, stream.cuda_stream),
+                      "mbs_maxpool_forward(stash)")
+        ctx.save_for_backward(idx)
+        ctx.geom = (n, c, h, w, k, code, c + c_extra)
+        return y, buf
+
+    @staticmethod
+    def backward(ctx, dy, dbuf):
+        (idx,) = ctx.saved_tensors
+        n, c, h, w, k, code, ctot = ctx.geom
+        dt = {_native.BF16: torch.bfloat16, _native.F32: torch.float32}[code]
+        if dy is None:
+            dy = torch.zeros((n, c, h // k, w // k), dtype=dt, device=idx.device, memory_format=torch.channels_last)
+        dy = dy.to(dt).contiguous(memory_format=torch.channels_last)
+        if dbuf is not None:
+            dbuf = dbuf.to(dt).contiguous(memory_format=torch.channels_last)
+        dx = torch.empty((n, c, h, w), dtype=dt, device=dy.device, memory_format=torch.channels_last)
+        stream = torch.cuda.current_stream(dy.device)
+        TIMER.launches += 1
+        _native.check(_native.lib().mbs_maxpool_backward(
+            dy.data_ptr(), idx.data_ptr(), dx.data_ptr(), code, n, h, w, c, k, k, 0,
+            None if dbuf is None else dbuf.data_ptr(), ctot, 0, stream.cuda_stream), "mbs_maxpool_backward(addend)")
+        return dx, None, None
+
+
+class _JoinFn(torch.autograd.Function):
+    """buf[:, C_s:] = up, in place (the second half of the U-Net concat); returns buf."""
+
+    @staticmethod
+    def forward(ctx, buf, up, c_skip):
+        buf[:, c_skip:].copy_(up)
+        ctx.mark_dirty(buf)
+        ctx.c_skip = c_skip
+        return buf
+
+    @staticmethod
+    def backward(ctx, g):
+        return g, g[:, ctx.c_skip:].contiguous(memory_format=torch.channels_last), None
+
+
+def pool_and_stash(s, kernel_size: int, c_extra: int):
+    """``(max_pool2d(s, k), buf)`` with ``buf[:, :C_s] = s`` — the U-Net skip written straight into the
+    decoder's concat buffer by the pooling kernel (non-overlapping k x k windows tiling s)."""
+    return _PoolStashFn.apply(s, int(kernel_size), int(c_extra))
+
+
+def join_skip(buf, up):
+    """Complete ``buf`` from :func:`pool_and_stash` with the upsampled tensor: equals ``torch.cat([s, up], 1)``."""
+    return _JoinFn.apply(buf, up, buf.shape[1] - up.shape[1])
 
 
 def max_pool2d(x, kernel_size: int, stride: int | None = None, padding: int = 0):
@@ -95,4 +166,4 @@ def swap_maxpool(model: nn.Module) -> nn.Module:
     return model
 
 
-__all__ = ["MicroMaxPool2d", "max_pool2d", "swap_maxpool", "supported"]
+__all__ = ["MicroMaxPool2d", "max_pool2d", "swap_maxpool", "supported", "pool_and_stash", "join_skip"]

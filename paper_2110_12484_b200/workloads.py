@@ -49,7 +49,11 @@ class UNet(nn.Module):
         self.pool = nn.MaxPool2d(2)
         self.outc = nn.Conv2d(64, out_channels, kernel_size=1)
 
+    native_skips = False   # set by build_model(ops="native"): skips written into the concat buffers by K6
+
     def forward(self, x):
+        if self.native_skips and x.is_cuda and x.shape[-2] % 16 == 0 and x.shape[-1] % 16 == 0:
+            return self._forward_native(x)
         skips = [self.inc(x)]
         for d in self.downs:
             skips.append(d(self.pool(skips[-1])))
@@ -57,6 +61,21 @@ class UNet(nn.Module):
         for u in self.ups:
             x = u(x, skips.pop())
         return self.outc(x)
+
+    def _forward_native(self, x):
+        """Same math; each skip is copied into its decoder concat buffer by the pooling kernel, the
+        upsampled half is joined in place, and the two gradients of a skip are summed inside the
+        pooling backward (pool.pool_and_stash / join_skip) — no torch.cat pass, no separate add."""
+        from .pool import join_skip, pool_and_stash
+        h = self.inc(x)
+        bufs = []
+        for d in self.downs:
+            pooled, buf = pool_and_stash(h, 2, h.shape[1])
+            bufs.append(buf)
+            h = d(pooled)
+        for u in self.ups:
+            h = u.conv(join_skip(bufs.pop(), u.up(h)))
+        return self.outc(h)
 
 
 @dataclass(frozen=True)
@@ -101,6 +120,8 @@ def build_model(w: Workload, ops: str = "torch") -> nn.Module:
         from .pool import swap_maxpool
         fuse_batchnorm(m)
         swap_maxpool(m)
+        if isinstance(m, UNet):
+            m.native_skips = True
     elif ops != "torch":
         raise ValueError(f"ops must be 'native' or 'torch', got {ops!r}")
     return m

@@ -76,3 +76,49 @@ def test_swapped_models_match_torch(cuda):
         x = torch.randn(shape, device=cuda).contiguous(memory_format=torch.channels_last)
         with torch.no_grad():
             assert torch.equal(net(x), sw(x))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_pool_and_stash_join_equal_cat(cuda, dtype):
+    """pool_and_stash + join_skip == (max_pool2d(s), cat([s, up])), gradients included (fp32: bit-exact)."""
+    g = torch.Generator(device=cuda).manual_seed(11)
+    s = torch.randn(2, 16, 12, 8, device=cuda, generator=g).to(dtype).contiguous(memory_format=torch.channels_last)
+    up = torch.randn(2, 16, 12, 8, device=cuda, generator=g).to(dtype).contiguous(memory_format=torch.channels_last)
+    w_p = torch.randn(2, 16, 6, 4, device=cuda, generator=g).to(dtype)
+    w_c = torch.randn(2, 32, 12, 8, device=cuda, generator=g).to(dtype)
+
+    def run(native):
+        sa = s.detach().clone().requires_grad_(True)
+        ua = up.detach().clone().requires_grad_(True)
+        if native:
+            p, buf = K6.pool_and_stash(sa, 2, 16)
+            c = K6.join_skip(buf, ua)
+        else:
+            p, c = F.max_pool2d(sa, 2), torch.cat([sa, ua], 1)
+        ((p.float() * w_p.float()).sum() + (c.float() * w_c.float()).sum()).backward()
+        return p.detach(), c.detach(), sa.grad, ua.grad
+
+    a, b = run(False), run(True)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[3], b[3])
+    if dtype == torch.float32:
+        assert torch.equal(a[2], b[2])
+    else:   # ours sums the two skip gradients in fp32 and rounds once (torch rounds twice)
+        assert (a[2].float() - b[2].float()).abs().max() <= 2 ** -7 * a[2].float().abs().max()
+
+
+def test_unet_native_skips_match_plain(cuda):
+    import copy
+    from paper_2110_12484_b200.workloads import UNet
+    torch.manual_seed(0)
+    net = UNet(3, 1).to(cuda).to(memory_format=torch.channels_last).train()
+    nat = copy.deepcopy(net)
+    nat.native_skips = True
+    x = torch.randn(2, 3, 32, 32, device=cuda).contiguous(memory_format=torch.channels_last)
+    outs = []
+    for m in (net, nat):
+        out = m(x)
+        (out ** 2).mean().backward()
+        outs.append((out.detach(), [p.grad.clone() for p in m.parameters()]))
+    assert torch.allclose(outs[0][0], outs[1][0], rtol=1e-5, atol=1e-6)
+    for ga, gb in zip(outs[0][1], outs[1][1]):
+        assert torch.allclose(ga, gb, rtol=1e-4, atol=1e-6)
