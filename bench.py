@@ -323,8 +323,15 @@ def main():
 
     # --- no-stream baseline: plain torch training at batch = micro, data resident ---
     nos = no_stream_baseline(w, dev, n_mu, args.steps, args.warmup, ws, ops=args.model_ops)
-    nos_torch = (no_stream_baseline(w, dev, n_mu, args.steps, args.warmup, ws, ops="torch")
-                 if args.model_ops != "torch" else None)
+    nos_torch = None
+    if args.model_ops != "torch":
+        b = n_mu        # the stock model holds more activations per sample: halve the batch until it fits
+        while b >= 1 and nos_torch is None:
+            try:
+                nos_torch = no_stream_baseline(w, dev, b, args.steps, args.warmup, ws, ops="torch")
+            except torch.OutOfMemoryError:
+                b //= 2
+            torch.cuda.empty_cache()
 
     # the reference's overhead report (streaming.py:130-149) on MEASURED schedules: the MBS step as
     # run (copy per micro from the streamer's events, compute per micro from the timed step) vs the
