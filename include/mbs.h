@@ -266,6 +266,20 @@ int mbs_maxpool_forward(const void* x, void* y, uint8_t* idx, int dtype, int64_t
 int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype, int64_t N, int64_t H, int64_t W,
                          int64_t C, int k, int s, int p, const void* addend, int64_t add_C, int64_t add_c0,
                          void* stream);
+/* Channel-slice copy between channels-last tensors seen as [M, C_total] rows:
+ * dst[m, dst_c0 + c] = src[m, src_c0 + c] (+ bias[c], fp32, nullable) for c < C (the U-Net skip join
+ * and its backward). */
+int mbs_copy_channels(const void* src, int64_t src_C, int64_t src_c0, void* dst, int64_t dst_C, int64_t dst_c0,
+                      int64_t M, int64_t C, const float* bias, int dtype, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Stem im2col (K7) — the model's first (3-channel) convolution as one library
+ * GEMM: cols[N*Ho*Wo, Kp] with column (kh*k + kw)*C + c = x[n, oh*s-p+kh,
+ * ow*s-p+kw, c] (0 outside the image), columns [k*k*C, Kp) zero. x channels-
+ * last [N,H,W,C]; dtype MBS_BF16 or MBS_F32; Kp >= k*k*C.
+ * ------------------------------------------------------------------------- */
+int mbs_im2col(const void* x, void* cols, int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int k, int s, int p,
+               int64_t Kp, void* stream);
 
 #ifdef __cplusplus
 }

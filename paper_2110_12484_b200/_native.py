@@ -82,6 +82,10 @@ _SIGS = {
                                     c_int, c_int, c_void_p, c_int64, c_int64, c_void_p]),
     "mbs_maxpool_backward": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64,
                                      c_int, c_int, c_int, c_void_p, c_int64, c_int64, c_void_p]),
+    "mbs_copy_channels": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p,
+                                  c_int, c_void_p]),
+    "mbs_im2col": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_int, c_int, c_int64,
+                           c_void_p]),
 }
 
 EXPORTS = tuple(_SIGS)

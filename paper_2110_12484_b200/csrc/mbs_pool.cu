@@ -208,6 +208,31 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
     }
 }
 
+// Channel-slice copy between channels-last tensors viewed as [M, C_total] rows:
+// dst[m, dc0 + c] = src[m, sc0 + c] (+ bias[c]) — the U-Net skip join (the upsampled half lands in
+// the concat buffer with its ConvTranspose bias added on the way) and its backward (the slice made
+// dense for the ConvTranspose backward). One thread per 16-byte vector; consecutive threads walk
+// consecutive channels, then rows.
+template <typename T, int V>
+__global__ void __launch_bounds__(kPoolThreads) k_copy_channels(const T* __restrict__ src, int64_t sC, int64_t sc0,
+                                                                T* __restrict__ dst, int64_t dC, int64_t dc0,
+                                                                int64_t M, int64_t C, const float* __restrict__ bias) {
+    cudaGridDependencySynchronize();
+    const int64_t cv = C / V;
+    const int64_t total = M * cv;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c0 = (t % cv) * V;
+        const int64_t m = t / cv;
+        float v[V];
+        PoolIO<T, V>::load(src + m * sC + sc0 + c0, v);
+        if (bias) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) v[i] += bias[c0 + i];
+        }
+        PoolIO<T, V>::store(dst + m * dC + dc0 + c0, v);
+    }
+}
+
 static int pool_sms() {
     static int n = 0;
     if (n <= 0) {
@@ -319,6 +344,35 @@ int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype
         else
             e = pool_launch(k_maxpool_bwd<float, 1>, ins * C, cs, (const float*)dy, idx, (float*)dx, g,
                             (const float*)addend, add_C, add_c0);
+    }
+    MBS_CK(e);
+    return MBS_OK;
+}
+
+int mbs_copy_channels(const void* src, int64_t src_C, int64_t src_c0, void* dst, int64_t dst_C, int64_t dst_c0,
+                      int64_t M, int64_t C, const float* bias, int dtype, void* stream) {
+    if (!src || !dst) return invalid("mbs_copy_channels: null pointer");
+    if (dtype != MBS_BF16 && dtype != MBS_F32) return invalid("mbs_copy_channels: dtype must be MBS_BF16 or MBS_F32");
+    if (M < 0 || C < 1 || src_c0 < 0 || dst_c0 < 0 || src_c0 + C > src_C || dst_c0 + C > dst_C)
+        return invalid("mbs_copy_channels: bad geometry");
+    if (M == 0) return MBS_OK;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    const int es = dtype == MBS_BF16 ? 2 : 4;
+    const int V = 16 / es;
+    const bool vec = C % V == 0 && src_C % V == 0 && dst_C % V == 0 && src_c0 % V == 0 && dst_c0 % V == 0 &&
+                     aligned16(src, dst, nullptr);
+    cudaError_t e;
+    if (dtype == MBS_BF16) {
+        using T = __nv_bfloat16;
+        e = vec ? pool_launch(k_copy_channels<T, 8>, M * (C / 8), cs, (const T*)src, src_C, src_c0, (T*)dst, dst_C, dst_c0,
+                              M, C, bias)
+                : pool_launch(k_copy_channels<T, 1>, M * C, cs, (const T*)src, src_C, src_c0, (T*)dst, dst_C, dst_c0, M,
+                              C, bias);
+    } else {
+        e = vec ? pool_launch(k_copy_channels<float, 4>, M * (C / 4), cs, (const float*)src, src_C, src_c0, (float*)dst,
+                              dst_C, dst_c0, M, C, bias)
+                : pool_launch(k_copy_channels<float, 1>, M * C, cs, (const float*)src, src_C, src_c0, (float*)dst, dst_C,
+                              dst_c0, M, C, bias);
     }
     MBS_CK(e);
     return MBS_OK;

@@ -109,19 +109,41 @@ class _PoolStashFn(torch.autograd.Function):
         return dx, None, None
 
 
+def _copy_channels(src, s_c, s_c0, dst, d_c, d_c0, m, c, bias):
+    stream = torch.cuda.current_stream(src.device)
+    TIMER.launches += 1
+    _native.check(_native.lib().mbs_copy_channels(src.data_ptr(), s_c, s_c0, dst.data_ptr(), d_c, d_c0, m, c,
+                                                  None if bias is None else bias.data_ptr(), _DTYPES[src.dtype],
+                                                  stream.cuda_stream), "mbs_copy_channels")
+
+
 class _JoinFn(torch.autograd.Function):
-    """buf[:, C_s:] = up, in place (the second half of the U-Net concat); returns buf."""
+    """buf[:, C_s:] = up (+ bias), in place (the second half of the U-Net concat); returns buf.
+
+    ``bias`` (fp32, nullable) is the ConvTranspose bias, added while copying instead of in a
+    separate broadcast pass over the upsampled tensor."""
 
     @staticmethod
-    def forward(ctx, buf, up, c_skip):
-        buf[:, c_skip:].copy_(up)
+    def forward(ctx, buf, up, bias, c_skip):
+        up = up.to(buf.dtype).contiguous(memory_format=torch.channels_last)
+        n, ctot, h, w = buf.shape
+        cu = ctot - c_skip
+        if bias is not None:
+            bias = bias.detach().float().contiguous()
+        _copy_channels(up, cu, 0, buf, ctot, c_skip, n * h * w, cu, bias)
         ctx.mark_dirty(buf)
-        ctx.c_skip = c_skip
+        ctx.geom = (n, ctot, h, w, c_skip, bias is not None)
         return buf
 
     @staticmethod
     def backward(ctx, g):
-        return g, g[:, ctx.c_skip:].contiguous(memory_format=torch.channels_last), None
+        n, ctot, h, w, cs, has_bias = ctx.geom
+        g = g.contiguous(memory_format=torch.channels_last)
+        cu = ctot - cs
+        gup = torch.empty((n, cu, h, w), dtype=g.dtype, device=g.device, memory_format=torch.channels_last)
+        _copy_channels(g, ctot, cs, gup, cu, 0, n * h * w, cu, None)
+        gb = gup.float().sum(dim=(0, 2, 3)) if has_bias and ctx.needs_input_grad[2] else None
+        return g, gup, gb, None
 
 
 def pool_and_stash(s, kernel_size: int, c_extra: int):
@@ -130,9 +152,10 @@ def pool_and_stash(s, kernel_size: int, c_extra: int):
     return _PoolStashFn.apply(s, int(kernel_size), int(c_extra))
 
 
-def join_skip(buf, up):
-    """Complete ``buf`` from :func:`pool_and_stash` with the upsampled tensor: equals ``torch.cat([s, up], 1)``."""
-    return _JoinFn.apply(buf, up, buf.shape[1] - up.shape[1])
+def join_skip(buf, up, bias=None):
+    """Complete ``buf`` from :func:`pool_and_stash` with the upsampled tensor (plus its per-channel
+    ``bias``, if given): equals ``torch.cat([s, up + bias], 1)``."""
+    return _JoinFn.apply(buf, up, bias, buf.shape[1] - up.shape[1])
 
 
 def max_pool2d(x, kernel_size: int, stride: int | None = None, padding: int = 0):

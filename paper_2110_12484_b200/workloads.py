@@ -74,7 +74,8 @@ class UNet(nn.Module):
             bufs.append(buf)
             h = d(pooled)
         for u in self.ups:
-            h = u.conv(join_skip(bufs.pop(), u.up(h)))
+            up = torch.nn.functional.conv_transpose2d(h, u.up.weight, None, u.up.stride, u.up.padding)
+            h = u.conv(join_skip(bufs.pop(), up, u.up.bias))   # bias added while joining
         return self.outc(h)
 
 
@@ -106,8 +107,10 @@ WORKLOADS = {
 
 
 def build_model(w: Workload, ops: str = "torch") -> nn.Module:
-    """The workload's model. ``ops="native"`` runs its BatchNorm(+ReLU/+skip add) on K5 (bn.py) and its
-    max-pools on K6 (pool.py); ``"torch"`` is the stock module. Parameters are identical either way."""
+    """The workload's model. ``ops="native"`` runs its BatchNorm(+ReLU/+skip add) on K5 (bn.py), its
+    max-pools on K6 (pool.py), its 3-channel stem conv as K7 im2col + cuBLAS GEMM and a 1x1 head
+    conv with < 8 outputs as one GEMM (stem.py);
+    ``"torch"`` is the stock module. Parameters are identical either way."""
     if w.model in ("resnet18", "resnet50"):
         import torchvision
         m = getattr(torchvision.models, w.model)(num_classes=w.n_classes)
@@ -118,8 +121,11 @@ def build_model(w: Workload, ops: str = "torch") -> nn.Module:
     if ops == "native":
         from .bn import fuse_batchnorm
         from .pool import swap_maxpool
+        from .stem import swap_pointwise, swap_stem
         fuse_batchnorm(m)
         swap_maxpool(m)
+        swap_stem(m)
+        swap_pointwise(m)
         if isinstance(m, UNet):
             m.native_skips = True
     elif ops != "torch":

@@ -9,6 +9,7 @@ import torchvision
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2110_12484_b200 import bn as K5  # noqa: E402
 from paper_2110_12484_b200 import pool as K6  # noqa: E402
+from paper_2110_12484_b200 import stem as K7  # noqa: E402
 from paper_2110_12484_b200.workloads import UNet  # noqa: E402
 
 
@@ -63,10 +64,14 @@ def models():
             if fused:
                 K5.fuse_batchnorm(m)
                 K6.swap_maxpool(m)
+                K7.swap_stem(m)
+                K7.swap_pointwise(m)
+                if hasattr(m, "native_skips"):
+                    m.native_skips = True
             x = torch.randn(shape, device=dev).to(memory_format=torch.channels_last)
             y = tgt(shape[0])
             ms, one = step_ms(m, x, y, lf)
-            print(f"{name} {'K5+K6 native' if fused else 'torch ops'}: {ms:.2f} ms/step "
+            print(f"{name} {'native ops' if fused else 'torch ops'}: {ms:.2f} ms/step "
                   f"({shape[0] / ms * 1000:.0f} samples/s)", flush=True)
             top_kernels(one)
             del m, x, y
