@@ -28,56 +28,53 @@ struct ColGeom {
 };
 
 constexpr int kColMaxKp = 512;
+constexpr int kColTileBytes = 16384;
 
-// One thread per 16-byte chunk (VE elements) of a cols row: consecutive threads write consecutive
-// chunks (fully coalesced stores); the (kh, kw, c) decomposition of each column comes from a
-// per-CTA smem table; the gathered input elements are L1/L2 hits (neighbouring output pixels
-// share most of their window).
-template <typename T, int VE>
-__global__ void __launch_bounds__(256) k_im2col(const T* __restrict__ x, T* __restrict__ cols, ColGeom g) {
-    __shared__ int16_t tdh[kColMaxKp], tdw[kColMaxKp], tc[kColMaxKp];
-    const int64_t K = (int64_t)g.k * g.k * g.C;
-    for (int j = threadIdx.x; j < g.Kp; j += blockDim.x) {
-        if (j < K) {
-            tdh[j] = (int16_t)(j / (g.k * g.C));
-            const int r = j % (g.k * (int)g.C);
-            tdw[j] = (int16_t)(r / g.C);
-            tc[j] = (int16_t)(r % g.C);
-        } else {
-            tdh[j] = -1;
-            tdw[j] = 0;
-            tc[j] = 0;
-        }
-    }
-    __syncthreads();
+// A CTA builds TM consecutive rows of cols in shared memory, then stores them as one contiguous
+// TM*Kp run with 16-byte coalesced stores. Filling: work item (kh, i) copies the k*C contiguous
+// input elements of kernel row kh for output pixel m0+i (consecutive threads take consecutive
+// pixels of the same kernel row, so their global reads are neighbours); padding columns are zeroed.
+// 32-bit index math (the host checks every offset fits).
+template <typename T>
+__global__ void __launch_bounds__(256) k_im2col(const T* __restrict__ x, T* __restrict__ cols, ColGeom g0, int TM) {
+    extern __shared__ __align__(16) unsigned char csm[];
+    T* tile = reinterpret_cast<T*>(csm);
+    const int H = (int)g0.H, W = (int)g0.W, C = (int)g0.C, Ho = (int)g0.Ho, Wo = (int)g0.Wo, Kp = (int)g0.Kp;
+    const int k = g0.k, s = g0.s, p = g0.p;
+    const int KC = k * C, K = k * KC;
+    const int64_t M = g0.N * g0.Ho * g0.Wo;
+    const int64_t n_tiles = (M + TM - 1) / TM;
     cudaGridDependencySynchronize();
-    const int64_t chunks = g.Kp / VE;
-    const int64_t total = g.N * g.Ho * g.Wo * chunks;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int j0 = (int)(t % chunks) * VE;
-        const int64_t m = t / chunks;
-        const int64_t ow = m % g.Wo;
-        const int64_t q = m / g.Wo;
-        const int64_t oh = q % g.Ho;
-        const int64_t n = q / g.Ho;
-        const int64_t h0 = oh * g.s - g.p, w0 = ow * g.s - g.p;
-        const T* base = x + n * g.H * g.W * g.C;
-        T v[VE];
-#pragma unroll
-        for (int e = 0; e < VE; ++e) {
-            const int j = j0 + e;
-            const int dh = tdh[j];
-            const int64_t ih = h0 + dh, iw = w0 + tdw[j];
-            v[e] = (dh >= 0 && ih >= 0 && ih < g.H && iw >= 0 && iw < g.W) ? base[(ih * g.W + iw) * g.C + tc[j]] : T(0.f);
+    for (int64_t tt = blockIdx.x; tt < n_tiles; tt += gridDim.x) {
+        const int64_t m0 = tt * TM;
+        const int rows = (int)min((int64_t)TM, M - m0);
+        for (int it = threadIdx.x; it < k * TM; it += blockDim.x) {
+            const int kh = it / TM, i = it - kh * TM;
+            if (i >= rows) continue;
+            const int m = (int)(m0 + i);
+            const int ow = m % Wo, q = m / Wo;
+            const int oh = q % Ho, n = q / Ho;
+            const int ih = oh * s - p + kh, iw0 = ow * s - p;
+            T* d = tile + i * Kp + kh * KC;
+            if (ih < 0 || ih >= H) {
+                for (int j = 0; j < KC; ++j) d[j] = T(0.f);
+            } else {
+                const T* src = x + ((size_t)(n * H + ih) * W) * C;
+                for (int kw = 0; kw < k; ++kw) {
+                    const int iw = iw0 + kw;
+                    const bool in = iw >= 0 && iw < W;
+                    for (int c = 0; c < C; ++c) d[kw * C + c] = in ? src[iw * C + c] : T(0.f);
+                }
+            }
+            if (kh == 0)
+                for (int j = K; j < Kp; ++j) tile[i * Kp + j] = T(0.f);
         }
-        if constexpr (sizeof(T) * VE == 16) {
-            uint4 u;
-            memcpy(&u, v, 16);
-            *reinterpret_cast<uint4*>(cols + m * g.Kp + j0) = u;
-        } else {
-#pragma unroll
-            for (int e = 0; e < VE; ++e) cols[m * g.Kp + j0 + e] = v[e];
-        }
+        __syncthreads();
+        const int64_t n16 = (int64_t)rows * Kp * sizeof(T) / 16;   // Kp*sizeof(T) is a multiple of 16
+        const uint4* s16 = reinterpret_cast<const uint4*>(tile);
+        uint4* d16 = reinterpret_cast<uint4*>(cols + m0 * Kp);
+        for (int64_t v = threadIdx.x; v < n16; v += blockDim.x) d16[v] = s16[v];
+        __syncthreads();
     }
 }
 
@@ -107,13 +104,18 @@ int mbs_im2col(const void* x, void* cols, int dtype, int64_t N, int64_t H, int64
     const int64_t Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
     if (Ho < 1 || Wo < 1) return invalid("mbs_im2col: window larger than input");
     ColGeom g{N, H, W, C, Ho, Wo, Kp, k, s, p};
-    const int ve = dtype == MBS_BF16 ? 8 : 4;
-    const bool vec = Kp % ve == 0 && !(reinterpret_cast<uintptr_t>(cols) & 15);
-    const int64_t work = N * Ho * Wo * (vec ? Kp / ve : Kp);
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 8LL * im2col_sms()));
+    const int es = dtype == MBS_BF16 ? 2 : 4;
+    if ((Kp * es) % 16 || (reinterpret_cast<uintptr_t>(cols) & 15))
+        return invalid("mbs_im2col: Kp * sizeof(elem) must be a multiple of 16 and cols 16-byte aligned");
+    if (N * H * W * C >= INT32_MAX || N * Ho * Wo >= INT32_MAX) return invalid("mbs_im2col: tensor too large");
+    const int TM = (int)std::max<int64_t>(32, kColTileBytes / (Kp * es));
+    const size_t smem = (size_t)TM * Kp * es;
+    const int64_t tiles = (N * Ho * Wo + TM - 1) / TM;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, 8LL * im2col_sms()));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = static_cast<cudaStream_t>(stream);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -121,12 +123,14 @@ int mbs_im2col(const void* x, void* cols, int dtype, int64_t N, int64_t H, int64
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e;
-    if (dtype == MBS_BF16)
-        e = vec ? cudaLaunchKernelEx(&cfg, k_im2col<__nv_bfloat16, 8>, (const __nv_bfloat16*)x, (__nv_bfloat16*)cols, g)
-                : cudaLaunchKernelEx(&cfg, k_im2col<__nv_bfloat16, 1>, (const __nv_bfloat16*)x, (__nv_bfloat16*)cols, g);
-    else
-        e = vec ? cudaLaunchKernelEx(&cfg, k_im2col<float, 4>, (const float*)x, (float*)cols, g)
-                : cudaLaunchKernelEx(&cfg, k_im2col<float, 1>, (const float*)x, (float*)cols, g);
+    if (dtype == MBS_BF16) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k_im2col<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)smem);
+        e = cudaLaunchKernelEx(&cfg, k_im2col<__nv_bfloat16>, (const __nv_bfloat16*)x, (__nv_bfloat16*)cols, g, TM);
+    } else {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k_im2col<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaLaunchKernelEx(&cfg, k_im2col<float>, (const float*)x, (float*)cols, g, TM);
+    }
     MBS_CK(e);
     return MBS_OK;
 }

@@ -66,6 +66,19 @@ struct PoolGeom {
     int k, s, p;
 };
 
+// Index math runs in 32 bits whenever every element offset fits (the 64-bit divisions of the
+// grid-stride decomposition dominated these memory-bound kernels: ncu, tools/k6_ncu.py).
+template <typename I>
+struct PoolGeomT {
+    I N, H, W, C, Ho, Wo;
+    int k, s, p;
+};
+
+template <typename I>
+static PoolGeomT<I> narrow(const PoolGeom& g) {
+    return PoolGeomT<I>{(I)g.N, (I)g.H, (I)g.W, (I)g.C, (I)g.Ho, (I)g.Wo, g.k, g.s, g.p};
+}
+
 template <int V>
 __device__ __forceinline__ void store_idx(uint8_t* p, const uint8_t (&v)[V]) {
     if constexpr (V == 8) {
@@ -102,21 +115,21 @@ __device__ __forceinline__ void load_idx(const uint8_t* p, uint8_t (&v)[V]) {
 // k | H, k | W) every input element is read exactly once, so the kernel also writes it into channel
 // columns [sc0, sc0 + C) of a wider channels-last tensor with row stride sC — the U-Net skip
 // connection lands in its concat buffer without a separate torch.cat pass.
-template <typename T, int V>
+template <typename T, int V, typename I>
 __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restrict__ x, T* __restrict__ y,
-                                                              uint8_t* __restrict__ idx, PoolGeom g,
-                                                              T* __restrict__ stash, int64_t sC, int64_t sc0) {
+                                                              uint8_t* __restrict__ idx, PoolGeomT<I> g,
+                                                              T* __restrict__ stash, I sC, I sc0) {
     cudaGridDependencySynchronize();
-    const int64_t cv = g.C / V;
-    const int64_t total = g.N * g.Ho * g.Wo * cv;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c0 = (t % cv) * V;
-        int64_t q = t / cv;
-        const int64_t ow = q % g.Wo;
+    const I cv = g.C / V;
+    const I total = g.N * g.Ho * g.Wo * cv;
+    for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
+        const I c0 = (t % cv) * V;
+        I q = t / cv;
+        const I ow = q % g.Wo;
         q /= g.Wo;
-        const int64_t oh = q % g.Ho;
-        const int64_t n = q / g.Ho;
-        const int64_t h0 = oh * g.s - g.p, w0 = ow * g.s - g.p;
+        const I oh = q % g.Ho;
+        const I n = q / g.Ho;
+        const I h0 = oh * g.s - g.p, w0 = ow * g.s - g.p;
         float m[V];
         uint8_t a[V];
 #pragma unroll
@@ -125,13 +138,13 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restric
             a[i] = 0;
         }
         for (int kh = 0; kh < g.k; ++kh) {
-            const int64_t ih = h0 + kh;
+            const I ih = h0 + kh;
             if (ih < 0 || ih >= g.H) continue;
             for (int kw = 0; kw < g.k; ++kw) {
-                const int64_t iw = w0 + kw;
+                const I iw = w0 + kw;
                 if (iw < 0 || iw >= g.W) continue;
                 float v[V];
-                const int64_t pix = (n * g.H + ih) * g.W + iw;
+                const I pix = (n * g.H + ih) * g.W + iw;
                 PoolIO<T, V>::load(x + pix * g.C + c0, v);
                 if (stash) PoolIO<T, V>::store(stash + pix * sC + sc0 + c0, v);
                 const uint8_t pos = (uint8_t)(kh * g.k + kw);
@@ -144,7 +157,7 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restric
                 }
             }
         }
-        const int64_t o = ((n * g.Ho + oh) * g.Wo + ow) * g.C + c0;
+        const I o = ((n * g.Ho + oh) * g.Wo + ow) * g.C + c0;
         PoolIO<T, V>::store(y + o, m);
         store_idx<V>(idx + o, a);
     }
@@ -153,54 +166,65 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restric
 // Optional addend: dx += add[pixel, ac0 + c] (row stride aC) in fp32 before the single rounding —
 // the gradient that reached the same tensor through the U-Net skip connection, fused instead of
 // autograd's separate add pass.
-template <typename T, int V>
+// W2: non-overlapping windows tiling the input (the U-Net 2x2/s2 pools) — no window search.
+template <typename T, int V, typename I, bool W2>
 __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restrict__ dy,
                                                               const uint8_t* __restrict__ idx, T* __restrict__ dx,
-                                                              PoolGeom g, const T* __restrict__ add, int64_t aC,
-                                                              int64_t ac0) {
+                                                              PoolGeomT<I> g, const T* __restrict__ add, I aC,
+                                                              I ac0) {
     cudaGridDependencySynchronize();
-    const int64_t cv = g.C / V;
-    const int64_t total = g.N * g.H * g.W * cv;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c0 = (t % cv) * V;
-        int64_t q = t / cv;
-        const int64_t iw = q % g.W;
+    const I cv = g.C / V;
+    const I total = g.N * g.H * g.W * cv;
+    for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
+        const I c0 = (t % cv) * V;
+        I q = t / cv;
+        const I iw = q % g.W;
         q /= g.W;
-        const int64_t ih = q % g.H;
-        const int64_t n = q / g.H;
+        const I ih = q % g.H;
+        const I n = q / g.H;
+        const I pix = (n * g.H + ih) * g.W + iw;
+        float a2[V];
+        if (add) PoolIO<T, V>::load(add + pix * aC + ac0 + c0, a2);   // independent of the windows: issue first
         // windows containing (ih, iw): oh*s - p <= ih <= oh*s - p + k - 1
-        const int64_t ohs = max((int64_t)0, (ih + g.p - g.k + g.s) / g.s);
-        const int64_t ohe = min(g.Ho, (ih + g.p) / g.s + 1);
-        const int64_t ows = max((int64_t)0, (iw + g.p - g.k + g.s) / g.s);
-        const int64_t owe = min(g.Wo, (iw + g.p) / g.s + 1);
+        const I ohs = max((I)0, (ih + g.p - g.k + g.s) / g.s);
+        const I ohe = min(g.Ho, (ih + g.p) / g.s + 1);
+        const I ows = max((I)0, (iw + g.p - g.k + g.s) / g.s);
+        const I owe = min(g.Wo, (iw + g.p) / g.s + 1);
         float acc[V];
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[i] = 0.f;
-        for (int64_t oh = ohs; oh < ohe; ++oh) {
-            const int kh = (int)(ih - (oh * g.s - g.p));
-            if (kh < 0 || kh >= g.k) continue;
-            for (int64_t ow = ows; ow < owe; ++ow) {
-                const int kw = (int)(iw - (ow * g.s - g.p));
-                if (kw < 0 || kw >= g.k) continue;
-                const uint8_t pos = (uint8_t)(kh * g.k + kw);
-                const int64_t o = ((n * g.Ho + oh) * g.Wo + ow) * g.C + c0;
-                uint8_t a[V];
-                load_idx<V>(idx + o, a);
-                bool any = false;
+        if constexpr (W2) {
+            // non-overlapping windows (k == s, p == 0): exactly one window per input element
+            const I oh = ih / g.s, ow = iw / g.s;
+            const uint8_t pos = (uint8_t)((ih - oh * g.s) * g.k + (iw - ow * g.s));
+            const I o = ((n * g.Ho + oh) * g.Wo + ow) * g.C + c0;
+            uint8_t a[V];
+            float d[V];
+            load_idx<V>(idx + o, a);
+            PoolIO<T, V>::load(dy + o, d);
 #pragma unroll
-                for (int i = 0; i < V; ++i) any |= a[i] == pos;
-                if (!any) continue;
-                float d[V];
-                PoolIO<T, V>::load(dy + o, d);
+            for (int i = 0; i < V; ++i)
+                if (a[i] == pos) acc[i] = d[i];
+        } else {
+            for (I oh = ohs; oh < ohe; ++oh) {
+                const int kh = (int)(ih - (oh * g.s - g.p));
+                if (kh < 0 || kh >= g.k) continue;
+                for (I ow = ows; ow < owe; ++ow) {
+                    const int kw = (int)(iw - (ow * g.s - g.p));
+                    if (kw < 0 || kw >= g.k) continue;
+                    const uint8_t pos = (uint8_t)(kh * g.k + kw);
+                    const I o = ((n * g.Ho + oh) * g.Wo + ow) * g.C + c0;
+                    uint8_t a[V];
+                    float d[V];
+                    load_idx<V>(idx + o, a);
+                    PoolIO<T, V>::load(dy + o, d);
 #pragma unroll
-                for (int i = 0; i < V; ++i)
-                    if (a[i] == pos) acc[i] += d[i];
+                    for (int i = 0; i < V; ++i)
+                        if (a[i] == pos) acc[i] += d[i];
+                }
             }
         }
-        const int64_t pix = (n * g.H + ih) * g.W + iw;
         if (add) {
-            float a2[V];
-            PoolIO<T, V>::load(add + pix * aC + ac0 + c0, a2);
 #pragma unroll
             for (int i = 0; i < V; ++i) acc[i] += a2[i];
         }
@@ -213,16 +237,16 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
 // the concat buffer with its ConvTranspose bias added on the way) and its backward (the slice made
 // dense for the ConvTranspose backward). One thread per 16-byte vector; consecutive threads walk
 // consecutive channels, then rows.
-template <typename T, int V>
-__global__ void __launch_bounds__(kPoolThreads) k_copy_channels(const T* __restrict__ src, int64_t sC, int64_t sc0,
-                                                                T* __restrict__ dst, int64_t dC, int64_t dc0,
-                                                                int64_t M, int64_t C, const float* __restrict__ bias) {
+template <typename T, int V, typename I>
+__global__ void __launch_bounds__(kPoolThreads) k_copy_channels(const T* __restrict__ src, I sC, I sc0,
+                                                                T* __restrict__ dst, I dC, I dc0,
+                                                                I M, I C, const float* __restrict__ bias) {
     cudaGridDependencySynchronize();
-    const int64_t cv = C / V;
-    const int64_t total = M * cv;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c0 = (t % cv) * V;
-        const int64_t m = t / cv;
+    const I cv = C / V;
+    const I total = M * cv;
+    for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
+        const I c0 = (t % cv) * V;
+        const I m = t / cv;
         float v[V];
         PoolIO<T, V>::load(src + m * sC + sc0 + c0, v);
         if (bias) {
@@ -233,21 +257,18 @@ __global__ void __launch_bounds__(kPoolThreads) k_copy_channels(const T* __restr
     }
 }
 
-static int pool_sms() {
-    static int n = 0;
-    if (n <= 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-    }
-    return n;
-}
 
 template <typename... KArgs, typename... Args>
 static cudaError_t pool_launch(void (*kernel)(KArgs...), int64_t work, cudaStream_t s, Args... args) {
     // grid-stride: at most 8 resident 256-thread CTAs per SM, fewer when the work is small
+    static int sms = 0;
+    if (sms <= 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
     const int64_t want = (work + kPoolThreads - 1) / kPoolThreads;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, 8LL * pool_sms()));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, 8LL * sms));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kPoolThreads);
@@ -275,6 +296,91 @@ static bool aligned16(const void* a, const void* b, const void* c) {
     return !((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(c)) & 15);
 }
 
+static bool fits_i32(int64_t v) { return v < (int64_t)INT32_MAX - (1 << 22); }  // grid-stride headroom
+
+template <typename I>
+static int maxpool_fwd(const void* x, void* y, uint8_t* idx, int dtype, const PoolGeom& g0, void* stash, int64_t sC,
+                       int64_t sc0, cudaStream_t cs) {
+    const PoolGeomT<I> g = narrow<I>(g0);
+    const int64_t outs = g0.N * g0.Ho * g0.Wo;
+    const int es = dtype == MBS_BF16 ? 2 : 4;
+    const bool stash_vec = !stash || (!(reinterpret_cast<uintptr_t>(stash) & 15) && (sC * es) % 16 == 0 &&
+                                      (sc0 * es) % 16 == 0);
+    const I isC = (I)sC, isc0 = (I)sc0;
+    cudaError_t e;
+    if (dtype == MBS_BF16) {
+        using T = __nv_bfloat16;
+        if (g0.C % 8 == 0 && aligned16(x, y, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7) && stash_vec)
+            e = pool_launch(k_maxpool_fwd<T, 8, I>, outs * (g0.C / 8), cs, (const T*)x, (T*)y, idx, g, (T*)stash, isC,
+                            isc0);
+        else
+            e = pool_launch(k_maxpool_fwd<T, 1, I>, outs * g0.C, cs, (const T*)x, (T*)y, idx, g, (T*)stash, isC, isc0);
+    } else {
+        if (g0.C % 4 == 0 && aligned16(x, y, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 3) && stash_vec)
+            e = pool_launch(k_maxpool_fwd<float, 4, I>, outs * (g0.C / 4), cs, (const float*)x, (float*)y, idx, g,
+                            (float*)stash, isC, isc0);
+        else
+            e = pool_launch(k_maxpool_fwd<float, 1, I>, outs * g0.C, cs, (const float*)x, (float*)y, idx, g,
+                            (float*)stash, isC, isc0);
+    }
+    MBS_CK(e);
+    return MBS_OK;
+}
+
+template <typename I, bool W2>
+static int maxpool_bwd(const void* dy, const uint8_t* idx, void* dx, int dtype, const PoolGeom& g0, const void* add,
+                       int64_t aC, int64_t ac0, cudaStream_t cs) {
+    const PoolGeomT<I> g = narrow<I>(g0);
+    const int64_t ins = g0.N * g0.H * g0.W;
+    const int es = dtype == MBS_BF16 ? 2 : 4;
+    const bool add_vec = !add || (!(reinterpret_cast<uintptr_t>(add) & 15) && (aC * es) % 16 == 0 &&
+                                  (ac0 * es) % 16 == 0);
+    const I iaC = (I)aC, iac0 = (I)ac0;
+    cudaError_t e;
+    if (dtype == MBS_BF16) {
+        using T = __nv_bfloat16;
+        if (g0.C % 8 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7) && add_vec)
+            e = pool_launch(k_maxpool_bwd<T, 8, I, W2>, ins * (g0.C / 8), cs, (const T*)dy, idx, (T*)dx, g, (const T*)add,
+                            iaC, iac0);
+        else
+            e = pool_launch(k_maxpool_bwd<T, 1, I, W2>, ins * g0.C, cs, (const T*)dy, idx, (T*)dx, g, (const T*)add, iaC,
+                            iac0);
+    } else {
+        if (g0.C % 4 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 3) && add_vec)
+            e = pool_launch(k_maxpool_bwd<float, 4, I, W2>, ins * (g0.C / 4), cs, (const float*)dy, idx, (float*)dx, g,
+                            (const float*)add, iaC, iac0);
+        else
+            e = pool_launch(k_maxpool_bwd<float, 1, I, W2>, ins * g0.C, cs, (const float*)dy, idx, (float*)dx, g,
+                            (const float*)add, iaC, iac0);
+    }
+    MBS_CK(e);
+    return MBS_OK;
+}
+
+template <typename I>
+static int copy_channels(const void* src, int64_t sC, int64_t sc0, void* dst, int64_t dC, int64_t dc0, int64_t M,
+                         int64_t C, const float* bias, int dtype, cudaStream_t cs) {
+    const int es = dtype == MBS_BF16 ? 2 : 4;
+    const int V = 16 / es;
+    const bool vec = C % V == 0 && sC % V == 0 && dC % V == 0 && sc0 % V == 0 && dc0 % V == 0 &&
+                     aligned16(src, dst, nullptr);
+    cudaError_t e;
+    if (dtype == MBS_BF16) {
+        using T = __nv_bfloat16;
+        e = vec ? pool_launch(k_copy_channels<T, 8, I>, M * (C / 8), cs, (const T*)src, (I)sC, (I)sc0, (T*)dst, (I)dC,
+                              (I)dc0, (I)M, (I)C, bias)
+                : pool_launch(k_copy_channels<T, 1, I>, M * C, cs, (const T*)src, (I)sC, (I)sc0, (T*)dst, (I)dC, (I)dc0,
+                              (I)M, (I)C, bias);
+    } else {
+        e = vec ? pool_launch(k_copy_channels<float, 4, I>, M * (C / 4), cs, (const float*)src, (I)sC, (I)sc0,
+                              (float*)dst, (I)dC, (I)dc0, (I)M, (I)C, bias)
+                : pool_launch(k_copy_channels<float, 1, I>, M * C, cs, (const float*)src, (I)sC, (I)sc0, (float*)dst,
+                              (I)dC, (I)dc0, (I)M, (I)C, bias);
+    }
+    MBS_CK(e);
+    return MBS_OK;
+}
+
 }  // namespace mbs
 
 using namespace mbs;
@@ -291,28 +397,10 @@ int mbs_maxpool_forward(const void* x, void* y, uint8_t* idx, int dtype, int64_t
         return invalid("mbs_maxpool_forward: a stash needs non-overlapping windows tiling the input (k == s, p == 0)");
     if (stash && (stash_c0 < 0 || stash_c0 + C > stash_C)) return invalid("mbs_maxpool_forward: stash columns");
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
-    const int64_t outs = g.N * g.Ho * g.Wo;
-    const int es = dtype == MBS_BF16 ? 2 : 4;
-    const bool stash_vec = !stash || (!(reinterpret_cast<uintptr_t>(stash) & 15) && (stash_C * es) % 16 == 0 &&
-                                      (stash_c0 * es) % 16 == 0);
-    cudaError_t e;
-    if (dtype == MBS_BF16) {
-        using T = __nv_bfloat16;
-        if (C % 8 == 0 && aligned16(x, y, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7) && stash_vec)
-            e = pool_launch(k_maxpool_fwd<T, 8>, outs * (C / 8), cs, (const T*)x, (T*)y, idx, g, (T*)stash, stash_C,
-                            stash_c0);
-        else
-            e = pool_launch(k_maxpool_fwd<T, 1>, outs * C, cs, (const T*)x, (T*)y, idx, g, (T*)stash, stash_C, stash_c0);
-    } else {
-        if (C % 4 == 0 && aligned16(x, y, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 3) && stash_vec)
-            e = pool_launch(k_maxpool_fwd<float, 4>, outs * (C / 4), cs, (const float*)x, (float*)y, idx, g,
-                            (float*)stash, stash_C, stash_c0);
-        else
-            e = pool_launch(k_maxpool_fwd<float, 1>, outs * C, cs, (const float*)x, (float*)y, idx, g, (float*)stash,
-                            stash_C, stash_c0);
-    }
-    MBS_CK(e);
-    return MBS_OK;
+    const bool i32 = fits_i32(g.N * g.H * g.W * std::max<int64_t>(g.C, stash ? stash_C : 0)) &&
+                     fits_i32(g.N * g.Ho * g.Wo * g.C);
+    return i32 ? maxpool_fwd<int32_t>(x, y, idx, dtype, g, stash, stash_C, stash_c0, cs)
+               : maxpool_fwd<int64_t>(x, y, idx, dtype, g, stash, stash_C, stash_c0, cs);
 }
 
 int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype, int64_t N, int64_t H, int64_t W,
@@ -324,29 +412,14 @@ int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype
     if (st) return st;
     if (addend && (add_c0 < 0 || add_c0 + C > add_C)) return invalid("mbs_maxpool_backward: addend columns");
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
-    const int64_t ins = g.N * g.H * g.W;
-    const int es = dtype == MBS_BF16 ? 2 : 4;
-    const bool add_vec = !addend || (!(reinterpret_cast<uintptr_t>(addend) & 15) && (add_C * es) % 16 == 0 &&
-                                     (add_c0 * es) % 16 == 0);
-    cudaError_t e;
-    if (dtype == MBS_BF16) {
-        using T = __nv_bfloat16;
-        if (C % 8 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7) && add_vec)
-            e = pool_launch(k_maxpool_bwd<T, 8>, ins * (C / 8), cs, (const T*)dy, idx, (T*)dx, g, (const T*)addend,
-                            add_C, add_c0);
-        else
-            e = pool_launch(k_maxpool_bwd<T, 1>, ins * C, cs, (const T*)dy, idx, (T*)dx, g, (const T*)addend, add_C,
-                            add_c0);
-    } else {
-        if (C % 4 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 3) && add_vec)
-            e = pool_launch(k_maxpool_bwd<float, 4>, ins * (C / 4), cs, (const float*)dy, idx, (float*)dx, g,
-                            (const float*)addend, add_C, add_c0);
-        else
-            e = pool_launch(k_maxpool_bwd<float, 1>, ins * C, cs, (const float*)dy, idx, (float*)dx, g,
-                            (const float*)addend, add_C, add_c0);
-    }
-    MBS_CK(e);
-    return MBS_OK;
+    const bool i32 = fits_i32(g.N * g.H * g.W * std::max<int64_t>(g.C, addend ? add_C : 0)) &&
+                     fits_i32(g.N * g.Ho * g.Wo * g.C);
+    const bool w2 = g.k == g.s && g.p == 0 && g.H % g.k == 0 && g.W % g.k == 0;   // one window per element
+    if (i32)
+        return w2 ? maxpool_bwd<int32_t, true>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs)
+                  : maxpool_bwd<int32_t, false>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs);
+    return w2 ? maxpool_bwd<int64_t, true>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs)
+              : maxpool_bwd<int64_t, false>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs);
 }
 
 int mbs_copy_channels(const void* src, int64_t src_C, int64_t src_c0, void* dst, int64_t dst_C, int64_t dst_c0,
@@ -357,25 +430,9 @@ int mbs_copy_channels(const void* src, int64_t src_C, int64_t src_c0, void* dst,
         return invalid("mbs_copy_channels: bad geometry");
     if (M == 0) return MBS_OK;
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
-    const int es = dtype == MBS_BF16 ? 2 : 4;
-    const int V = 16 / es;
-    const bool vec = C % V == 0 && src_C % V == 0 && dst_C % V == 0 && src_c0 % V == 0 && dst_c0 % V == 0 &&
-                     aligned16(src, dst, nullptr);
-    cudaError_t e;
-    if (dtype == MBS_BF16) {
-        using T = __nv_bfloat16;
-        e = vec ? pool_launch(k_copy_channels<T, 8>, M * (C / 8), cs, (const T*)src, src_C, src_c0, (T*)dst, dst_C, dst_c0,
-                              M, C, bias)
-                : pool_launch(k_copy_channels<T, 1>, M * C, cs, (const T*)src, src_C, src_c0, (T*)dst, dst_C, dst_c0, M,
-                              C, bias);
-    } else {
-        e = vec ? pool_launch(k_copy_channels<float, 4>, M * (C / 4), cs, (const float*)src, src_C, src_c0, (float*)dst,
-                              dst_C, dst_c0, M, C, bias)
-                : pool_launch(k_copy_channels<float, 1>, M * C, cs, (const float*)src, src_C, src_c0, (float*)dst, dst_C,
-                              dst_c0, M, C, bias);
-    }
-    MBS_CK(e);
-    return MBS_OK;
+    const bool i32 = fits_i32(M * std::max(src_C, dst_C));
+    return i32 ? copy_channels<int32_t>(src, src_C, src_c0, dst, dst_C, dst_c0, M, C, bias, dtype, cs)
+               : copy_channels<int64_t>(src, src_C, src_c0, dst, dst_C, dst_c0, M, C, bias, dtype, cs);
 }
 
 }  // extern "C"
