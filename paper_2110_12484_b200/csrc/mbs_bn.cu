@@ -26,12 +26,17 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <map>
 #include <mutex>
 
 #include "mbs_common.h"
 #include "mbs_tma.h"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace mbs {
 
@@ -115,18 +120,17 @@ __device__ __forceinline__ float relu_mask(float x, float sc, float sh, float r,
 // MODE 0: statistics — partial (sum(x-K), sum((x-K)^2)).
 // MODE 1: backward reduce — partial (sum g, sum g*(x-mean)), g = dy * relu-mask.
 template <typename T, int V, int MODE, bool RELU, bool RES>
-__global__ void __launch_bounds__(kBnThreads) k_bn_reduce(const T* __restrict__ x, const T* __restrict__ dy,
+__device__ __forceinline__ void bn_reduce_body(const T* __restrict__ x, const T* __restrict__ dy,
                                                           const T* __restrict__ res, const float* __restrict__ w,
                                                           const float* __restrict__ b,
                                                           const float* __restrict__ mean,
                                                           const float* __restrict__ invstd, float2* __restrict__ part,
-                                                          BnGeom g) {
+                                                          BnGeom g, int bx, int by){
     __shared__ float red[2][kBnThreads * V];
     const int tid = threadIdx.x;
     const int lane = tid % g.gv, rph = tid / g.gv;
-    const int64_t c0 = ((int64_t)blockIdx.y * g.gv + lane) * V;
+    const int64_t c0 = ((int64_t)by * g.gv + lane) * V;
     const bool active = rph < g.rp && c0 < g.C;
-    cudaGridDependencySynchronize();  // PDL: x / dy come from the preceding kernel
     float s1[V], s2[V], k[V], sc[V], sh[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) { s1[i] = 0.f; s2[i] = 0.f; k[i] = 0.f; sc[i] = 0.f; sh[i] = 0.f; }
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_reduce(const T* __restrict__ 
                 if (RELU) bn_affine(w, b, mean, invstd, c0 + i, sc[i], sh[i]);
             }
         }
-        const int64_t r0 = (int64_t)blockIdx.x * g.chunk;
+        const int64_t r0 = (int64_t)bx * g.chunk;
         const int64_t r1 = min(g.rows, r0 + g.chunk);
         constexpr int U = MODE == 0 ? 8 : 4;  // statistics: one stream, more loads in flight per thread
         int64_t r = r0 + rph;
@@ -205,15 +209,26 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_reduce(const T* __restrict__ 
     __syncthreads();
     const int gc = g.gv * V;  // channels in this group
     for (int j = tid; j < gc; j += kBnThreads) {
-        const int64_t c = (int64_t)blockIdx.y * gc + j;
+        const int64_t c = (int64_t)by * gc + j;
         if (c >= g.C) break;
         float a = 0.f, q = 0.f;
         for (int p = 0; p < g.rp; ++p) {
             a += red[0][p * gc + j];
             q += red[1][p * gc + j];
         }
-        part[c * g.P + blockIdx.x] = make_float2(a, q);
+        part[c * g.P + bx] = make_float2(a, q);
     }
+}
+
+template <typename T, int V, int MODE, bool RELU, bool RES>
+__global__ void __launch_bounds__(kBnThreads) k_bn_reduce(const T* __restrict__ x, const T* __restrict__ dy,
+                                                          const T* __restrict__ res, const float* __restrict__ w,
+                                                          const float* __restrict__ b,
+                                                          const float* __restrict__ mean,
+                                                          const float* __restrict__ invstd, float2* __restrict__ part,
+                                                          BnGeom g) {
+    cudaGridDependencySynchronize();  // PDL: inputs come from the preceding kernel
+    bn_reduce_body<T, V, MODE, RELU, RES>(x, dy, res, w, b, mean, invstd, part, g, blockIdx.x, blockIdx.y);
 }
 
 // TPC threads per channel (power of two, 32..256) merge the P CTA partials in fp64: thread j
@@ -257,6 +272,30 @@ __device__ __forceinline__ bool group_merge(const float2* part, int P, bool vali
     return valid && t == 0;
 }
 
+template <typename T>
+__device__ __forceinline__ void bn_stats_write(const T* __restrict__ x, const BnGeom& g, const float* __restrict__ w,
+                                               const float* __restrict__ b, float* running_mean, float* running_var,
+                                               double momentum, double eps, float* __restrict__ save_mean,
+                                               float* __restrict__ save_invstd, float* __restrict__ coef, int64_t c,
+                                               double s1, double s2) {
+    const double m = (double)g.rows;
+    const double K = (double)static_cast<float>(x[c]);
+    const double dm = s1 / m;
+    const double var = fmax(s2 / m - dm * dm, 0.0);  // biased: normalisation uses it (nn.py:278)
+    const double mean = K + dm;
+    save_mean[c] = (float)mean;
+    save_invstd[c] = (float)(1.0 / sqrt(var + eps));
+    if (running_mean) {
+        running_mean[c] = (float)((1.0 - momentum) * (double)running_mean[c] + momentum * mean);
+        const double unbiased = g.rows > 1 ? var * m / (m - 1.0) : var;
+        running_var[c] = (float)((1.0 - momentum) * (double)running_var[c] + momentum * unbiased);
+    }
+    float sc, sh;
+    bn_affine(w, b, save_mean, save_invstd, c, sc, sh);
+    coef[2 * c] = sc;
+    coef[2 * c + 1] = sh;
+}
+
 template <typename T, int TPC>
 __global__ void __launch_bounds__(kBnThreads) k_bn_stats_finalize(
         const T* __restrict__ x, const float2* __restrict__ part, BnGeom g, const float* __restrict__ w,
@@ -265,29 +304,29 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_stats_finalize(
     const int64_t c = (int64_t)blockIdx.x * (kBnThreads / TPC) + threadIdx.x / TPC;
     cudaGridDependencySynchronize();  // PDL: partials come from the statistics kernel
     double s1, s2;
-    if (group_merge<TPC>(part + c * g.P, g.P, c < g.C, s1, s2)) {
-        const double m = (double)g.rows;
-        const double K = (double)static_cast<float>(x[c]);
-        const double dm = s1 / m;
-        const double var = fmax(s2 / m - dm * dm, 0.0);  // biased: normalisation uses it (nn.py:278)
-        const double mean = K + dm;
-        save_mean[c] = (float)mean;
-        save_invstd[c] = (float)(1.0 / sqrt(var + eps));
-        if (running_mean) {
-            running_mean[c] = (float)((1.0 - momentum) * (double)running_mean[c] + momentum * mean);
-            const double unbiased = g.rows > 1 ? var * m / (m - 1.0) : var;
-            running_var[c] = (float)((1.0 - momentum) * (double)running_var[c] + momentum * unbiased);
-        }
-        float sc, sh;
-        bn_affine(w, b, save_mean, save_invstd, c, sc, sh);
-        coef[2 * c] = sc;
-        coef[2 * c + 1] = sh;
-    }
+    if (group_merge<TPC>(part + c * g.P, g.P, c < g.C, s1, s2))
+        bn_stats_write(x, g, w, b, running_mean, running_var, momentum, eps, save_mean, save_invstd, coef, c, s1, s2);
 }
 
 // backward finalize: dgamma = invstd * sum g(x-mean), dbeta = sum g; dx coefficients
 // dx = k1*g + A*(x-mean) + B with k1 = gamma*invstd, A = -k1*invstd*dgamma/M, B = -k1*dbeta/M
 // (stored: A, B, B - A*mean).
+__device__ __forceinline__ void bn_bwd_write(const BnGeom& g, const float* __restrict__ w,
+                                             const float* __restrict__ mean, const float* __restrict__ invstd,
+                                             float* __restrict__ dweight, float* __restrict__ dbias,
+                                             float* __restrict__ coef, int64_t c, double sg, double sgx) {
+    const double is = (double)invstd[c];
+    const double dgam = sgx * is;
+    if (dweight) dweight[c] = (float)dgam;
+    if (dbias) dbias[c] = (float)sg;
+    const double m = (double)g.rows;
+    const double k1 = (w ? (double)w[c] : 1.0) * is;
+    const double A = -k1 * is * dgam / m, B = -k1 * sg / m;
+    coef[3 * c] = (float)A;
+    coef[3 * c + 1] = (float)B;
+    coef[3 * c + 2] = (float)(B - A * (double)mean[c]);
+}
+
 template <int TPC>
 __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_finalize(
         const float2* __restrict__ part, BnGeom g, const float* __restrict__ w, const float* __restrict__ mean,
@@ -296,27 +335,16 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_finalize(
     const int64_t c = (int64_t)blockIdx.x * (kBnThreads / TPC) + threadIdx.x / TPC;
     cudaGridDependencySynchronize();  // PDL: partials come from the backward reduce kernel
     double sg, sgx;
-    if (group_merge<TPC>(part + c * g.P, g.P, c < g.C, sg, sgx)) {
-        const double is = (double)invstd[c];
-        const double dgam = sgx * is;
-        if (dweight) dweight[c] = (float)dgam;
-        if (dbias) dbias[c] = (float)sg;
-        const double m = (double)g.rows;
-        const double k1 = (w ? (double)w[c] : 1.0) * is;
-        const double A = -k1 * is * dgam / m, B = -k1 * sg / m;
-        coef[3 * c] = (float)A;
-        coef[3 * c + 1] = (float)B;
-        coef[3 * c + 2] = (float)(B - A * (double)mean[c]);
-    }
+    if (group_merge<TPC>(part + c * g.P, g.P, c < g.C, sg, sgx))
+        bn_bwd_write(g, w, mean, invstd, dweight, dbias, coef, c, sg, sgx);
 }
 
 template <typename T, int V, bool RELU, bool RES>
-__global__ void __launch_bounds__(kBnThreads) k_bn_apply(const T* __restrict__ x, const T* __restrict__ res,
-                                                         T* __restrict__ y, const float* __restrict__ coef, BnGeom g) {
+__device__ __forceinline__ void bn_apply_body(const T* __restrict__ x, const T* __restrict__ res,
+                                                         T* __restrict__ y, const float* __restrict__ coef, BnGeom g, int bx, int by){
     const int tid = threadIdx.x;
     const int lane = tid % g.gv, rph = tid / g.gv;
-    const int64_t c0 = ((int64_t)blockIdx.y * g.gv + lane) * V;
-    cudaGridDependencySynchronize();  // PDL: coef comes from the finalize kernel
+    const int64_t c0 = ((int64_t)by * g.gv + lane) * V;
     if (rph >= g.rp || c0 >= g.C) return;
     float sc[V], sh[V];
 #pragma unroll
@@ -324,7 +352,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_apply(const T* __restrict__ x
         sc[i] = coef[2 * (c0 + i)];
         sh[i] = coef[2 * (c0 + i) + 1];
     }
-    const int64_t r0 = (int64_t)blockIdx.x * g.chunk;
+    const int64_t r0 = (int64_t)bx * g.chunk;
     const int64_t r1 = min(g.rows, r0 + g.chunk);
     constexpr int U = 4;
     int64_t r = r0 + rph;
@@ -360,23 +388,29 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_apply(const T* __restrict__ x
     }
 }
 
+template <typename T, int V, bool RELU, bool RES>
+__global__ void __launch_bounds__(kBnThreads) k_bn_apply(const T* __restrict__ x, const T* __restrict__ res,
+                                                         T* __restrict__ y, const float* __restrict__ coef, BnGeom g) {
+    cudaGridDependencySynchronize();  // PDL: inputs come from the preceding kernel
+    bn_apply_body<T, V, RELU, RES>(x, res, y, coef, g, blockIdx.x, blockIdx.y);
+}
+
 // dx = k1*g + A*(x-mean) + B, g = dy * mask; with a residual, dres = g. k1 = gamma*invstd is
 // bit-identical to the forward scale (a float product; the fp64 product of two floats rounds to
 // the same value). bf16 activations use the folded dx = k1*g + (A*x + (B - A*mean)): the fp32
 // rounding of A*x (~6e-8 |A*mean|) is far below the bf16 output ulp, and it frees V registers.
 template <typename T, int V, bool RELU, bool RES>
-__global__ void __launch_bounds__(kBnThreads) k_bn_bwd_elemt(const T* __restrict__ x, const T* __restrict__ dy,
+__device__ __forceinline__ void bn_elemt_body(const T* __restrict__ x, const T* __restrict__ dy,
                                                              const T* __restrict__ res, T* __restrict__ dx,
                                                              T* __restrict__ dres, const float* __restrict__ w,
                                                              const float* __restrict__ b,
                                                              const float* __restrict__ mean,
                                                              const float* __restrict__ invstd,
-                                                             const float* __restrict__ coef, BnGeom g) {
+                                                             const float* __restrict__ coef, BnGeom g, int bx, int by){
     constexpr bool kFold = sizeof(T) == 2;
     const int tid = threadIdx.x;
     const int lane = tid % g.gv, rph = tid / g.gv;
-    const int64_t c0 = ((int64_t)blockIdx.y * g.gv + lane) * V;
-    cudaGridDependencySynchronize();  // PDL: coef comes from the finalize kernel
+    const int64_t c0 = ((int64_t)by * g.gv + lane) * V;
     if (rph >= g.rp || c0 >= g.C) return;
     float A[V], B[V], mu[V], sc[V], sh[V];
 #pragma unroll
@@ -386,7 +420,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_elemt(const T* __restrict
         mu[i] = kFold ? 0.f : mean[c0 + i];
         bn_affine(w, b, mean, invstd, c0 + i, sc[i], sh[i]);
     }
-    const int64_t r0 = (int64_t)blockIdx.x * g.chunk;
+    const int64_t r0 = (int64_t)bx * g.chunk;
     const int64_t r1 = min(g.rows, r0 + g.chunk);
     constexpr int U = 2;
     int64_t r = r0 + rph;
@@ -420,6 +454,70 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_elemt(const T* __restrict
         if (RELU && RES) BnIO<T, V>::load(res + o, rv);
         body(xv, dv, rv, o);
     }
+}
+
+template <typename T, int V, bool RELU, bool RES>
+__global__ void __launch_bounds__(kBnThreads) k_bn_bwd_elemt(const T* __restrict__ x, const T* __restrict__ dy,
+                                                             const T* __restrict__ res, T* __restrict__ dx,
+                                                             T* __restrict__ dres, const float* __restrict__ w,
+                                                             const float* __restrict__ b,
+                                                             const float* __restrict__ mean,
+                                                             const float* __restrict__ invstd,
+                                                             const float* __restrict__ coef, BnGeom g) {
+    cudaGridDependencySynchronize();  // PDL: inputs come from the preceding kernel
+    bn_elemt_body<T, V, RELU, RES>(x, dy, res, dx, dres, w, b, mean, invstd, coef, g, blockIdx.x, blockIdx.y);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Cooperative single-kernel path for the smallest BatchNorm layers: reduce -> grid barrier ->
+// per-channel finalize (a warp per channel, grid-strided) -> grid barrier -> apply / elemt over the
+// CTA's own rows, which it read moments ago (L2 hits). Removes two kernel boundaries and the
+// separate finalize launch per direction. Measured (profiles/r01_k5_fused_ab.txt, ResNet-50 step):
+// with PDL already hiding most launch gaps, limits of 0 / 8 / 16 MB are within 0.4 % of each other
+// and 32 / 64 MB are slower (the grid barriers and the register-path apply cost more than the
+// saved launches on mid-size layers), so only layers <= 8 MB take it. Same arithmetic as the
+// three-kernel path; the partial grouping (grid size) may differ, so agreement is to fp32 noise.
+// ---------------------------------------------------------------------------------------------
+template <typename T, int V, bool RELU, bool RES>
+__global__ void __launch_bounds__(kBnThreads) k_bn_fused_fwd(
+        const T* __restrict__ x, const T* __restrict__ res, T* __restrict__ y, const float* __restrict__ w,
+        const float* __restrict__ b, float* running_mean, float* running_var, double momentum, double eps,
+        float* __restrict__ save_mean, float* __restrict__ save_invstd, float* __restrict__ coef,
+        float2* __restrict__ part, BnGeom g) {
+    cg::grid_group grid = cg::this_grid();
+    cudaGridDependencySynchronize();
+    bn_reduce_body<T, V, 0, false, false>(x, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, part, g,
+                                          blockIdx.x, 0);
+    grid.sync();
+    const int warp = threadIdx.x / 32, wpb = kBnThreads / 32;
+    for (int64_t c = (int64_t)blockIdx.x * wpb + warp; c < g.C; c += (int64_t)gridDim.x * wpb) {
+        double s1, s2;
+        if (group_merge<32>(part + c * g.P, g.P, true, s1, s2))
+            bn_stats_write(x, g, w, b, running_mean, running_var, momentum, eps, save_mean, save_invstd, coef, c, s1,
+                           s2);
+    }
+    grid.sync();
+    bn_apply_body<T, V, RELU, RES>(x, res, y, coef, g, blockIdx.x, 0);
+}
+
+template <typename T, int V, bool RELU, bool RES>
+__global__ void __launch_bounds__(kBnThreads) k_bn_fused_bwd(
+        const T* __restrict__ x, const T* __restrict__ dy, const T* __restrict__ res, T* __restrict__ dx,
+        T* __restrict__ dres, const float* __restrict__ w, const float* __restrict__ b, const float* __restrict__ mean,
+        const float* __restrict__ invstd, float* __restrict__ dweight, float* __restrict__ dbias,
+        float* __restrict__ coef, float2* __restrict__ part, BnGeom g) {
+    cg::grid_group grid = cg::this_grid();
+    cudaGridDependencySynchronize();
+    bn_reduce_body<T, V, 1, RELU, RES>(x, dy, res, w, b, mean, invstd, part, g, blockIdx.x, 0);
+    grid.sync();
+    const int warp = threadIdx.x / 32, wpb = kBnThreads / 32;
+    for (int64_t c = (int64_t)blockIdx.x * wpb + warp; c < g.C; c += (int64_t)gridDim.x * wpb) {
+        double sg, sgx;
+        if (group_merge<32>(part + c * g.P, g.P, true, sg, sgx))
+            bn_bwd_write(g, w, mean, invstd, dweight, dbias, coef, c, sg, sgx);
+    }
+    grid.sync();
+    bn_elemt_body<T, V, RELU, RES>(x, dy, res, dx, dres, w, b, mean, invstd, coef, g, blockIdx.x, 0);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -751,6 +849,93 @@ static cudaError_t launch_tma(const T* X, const T* DY, const T* R, T* OUT, T* DR
 
 static bool tma_ok(int64_t C, int V) { return V > 1 && C / V <= kBnThreads; }
 
+constexpr int64_t kFusedMaxBytes = 8LL << 20;  // A/B: 0 / 8 / 16 MB within 0.4 %; larger limits were slower
+
+static int64_t fused_max_bytes() {  // A/B: MBS_K5_FUSED_MB overrides the size limit of the cooperative path
+    const char* e = getenv("MBS_K5_FUSED_MB");
+    return e ? (int64_t)atoll(e) << 20 : kFusedMaxBytes;
+}
+
+static int fused_mode() {  // A/B and tests: MBS_K5_FUSED=0 selects the three-kernel path
+    const char* e = getenv("MBS_K5_FUSED");
+    return e ? atoi(e) : 1;
+}
+
+// Cooperative launch (every CTA resident: grid <= occupancy x SMs), with PDL when the driver accepts
+// the combination (checked once per kernel). coop_geometry() sizes the grid first (the geometry is
+// a kernel argument), coop_launch() launches it.
+struct CoopInfo {
+    int resident;
+    int pdl;
+};
+static std::mutex g_coop_mu;
+static std::map<const void*, CoopInfo> g_coop;
+
+template <typename K>
+static CoopInfo coop_info(K kernel) {
+    std::lock_guard<std::mutex> lock(g_coop_mu);
+    auto it = g_coop.find((const void*)kernel);
+    if (it == g_coop.end()) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBnThreads, 0) != cudaSuccess) per_sm = 0;
+        it = g_coop.emplace((const void*)kernel, CoopInfo{per_sm * sm_count(), 1}).first;
+    }
+    return it->second;
+}
+
+template <typename K>
+static bool coop_geometry(K kernel, BnGeom& g, int V) {
+    const CoopInfo info = coop_info(kernel);
+    if (info.resident < 1) return false;
+    g = bn_geom(g.rows, g.C, V, 16, std::min(info.resident, kMaxReduceCtas));
+    return true;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t coop_launch(void (*kernel)(KArgs...), int grid, cudaStream_t s, Args... args) {
+    const CoopInfo info = coop_info(kernel);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBnThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = info.pdl ? 2 : 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+    if (e != cudaSuccess && info.pdl) {  // PDL + cooperative refused: remember, retry cooperative only
+        cudaGetLastError();
+        {
+            std::lock_guard<std::mutex> lock(g_coop_mu);
+            g_coop[(const void*)kernel].pdl = 0;
+        }
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+    }
+    return e;
+}
+
+template <typename T, int V, bool RELU, bool RES>
+static cudaError_t fused_fwd(const T* X, const T* R, T* Y, const float* w, const float* b, float* rm, float* rv,
+                             double momentum, double eps, float* smean, float* sinv, float* coef, float2* part,
+                             BnGeom g, cudaStream_t s) {
+    auto k = k_bn_fused_fwd<T, V, RELU, RES>;
+    if (!coop_geometry(k, g, V)) return cudaErrorCooperativeLaunchTooLarge;
+    return coop_launch(k, g.P, s, X, R, Y, w, b, rm, rv, momentum, eps, smean, sinv, coef, part, g);
+}
+
+template <typename T, int V, bool RELU, bool RES>
+static cudaError_t fused_bwd(const T* X, const T* DY, const T* R, T* DX, T* DR, const float* w, const float* b,
+                             const float* smean, const float* sinv, float* dw, float* db, float* coef, float2* part,
+                             BnGeom g, cudaStream_t s) {
+    auto k = k_bn_fused_bwd<T, V, RELU, RES>;
+    if (!coop_geometry(k, g, V)) return cudaErrorCooperativeLaunchTooLarge;
+    return coop_launch(k, g.P, s, X, DY, R, DX, DR, w, b, smean, sinv, dw, db, coef, part, g);
+}
+
 template <typename T, int V>
 static int bn_forward_t(const void* x, const void* res, void* y, int64_t rows, int64_t C, const float* w,
                         const float* b, float* rm, float* rv, double momentum, double eps, int relu, float* smean,
@@ -764,6 +949,17 @@ static int bn_forward_t(const void* x, const void* res, void* y, int64_t rows, i
     g.rows = rows;
     g.C = C;
     const bool tma = tma_ok(C, V);
+    if (tma && fused_mode() && rows * C * (int64_t)sizeof(T) <= fused_max_bytes()) {
+        cudaError_t e;
+        if (relu && res)
+            e = fused_fwd<T, V, true, true>(X, R, Y, w, b, rm, rv, momentum, eps, smean, sinv, coef, part, g, s);
+        else if (relu)
+            e = fused_fwd<T, V, true, false>(X, R, Y, w, b, rm, rv, momentum, eps, smean, sinv, coef, part, g, s);
+        else
+            e = fused_fwd<T, V, false, false>(X, R, Y, w, b, rm, rv, momentum, eps, smean, sinv, coef, part, g, s);
+        MBS_CK(e);
+        return MBS_OK;
+    }
     // statistics: the register-pipelined kernel (ncu A/B on B200: 40 us vs 48 us through the bulk-async
     // ring for a 205 MB single read-only stream); apply / backward use the ring.
     MBS_CK((launch_reduce<T, V, 0, false, false>(X, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, part, g,
@@ -803,6 +999,18 @@ static int bn_backward_t(const void* x, const void* res, const void* dy, void* d
     g.C = C;
     cudaError_t e;
     const bool tma = tma_ok(C, V);
+    T* DX = static_cast<T*>(dx);
+    T* DR = static_cast<T*>(dres);
+    if (tma && fused_mode() && rows * C * (int64_t)sizeof(T) * (2 + (res ? 1 : 0)) <= fused_max_bytes()) {
+        if (relu && res)
+            e = fused_bwd<T, V, true, true>(X, DY, R, DX, DR, w, b, smean, sinv, dw, db, coef, part, g, s);
+        else if (relu)
+            e = fused_bwd<T, V, true, false>(X, DY, R, DX, DR, w, b, smean, sinv, dw, db, coef, part, g, s);
+        else
+            e = fused_bwd<T, V, false, false>(X, DY, R, DX, DR, w, b, smean, sinv, dw, db, coef, part, g, s);
+        MBS_CK(e);
+        return MBS_OK;
+    }
     if (tma && relu && res)
         e = launch_tma<T, V, 1, true, true>(X, DY, R, nullptr, nullptr, w, b, smean, sinv, nullptr, part, g, s);
     else if (tma && relu)
@@ -819,8 +1027,6 @@ static int bn_backward_t(const void* x, const void* res, const void* dy, void* d
     else if (tpc == 128) e = launch_bwd_finalize<128>(part, g, w, smean, sinv, dw, db, coef, s);
     else e = launch_bwd_finalize<256>(part, g, w, smean, sinv, dw, db, coef, s);
     MBS_CK(e);
-    T* DX = static_cast<T*>(dx);
-    T* DR = static_cast<T*>(dres);
     BnGeom ge = g;
     if (tma && relu && res)
         e = launch_tma<T, V, 3, true, true>(X, DY, R, DX, DR, w, b, smean, sinv, coef, nullptr, ge, s);
