@@ -201,11 +201,12 @@ def test_fused_model_no_worse_than_torch_model_fp32(cuda, idx):
 @pytest.mark.parametrize("shape", [(32, 64, 28, 28), (16, 2048, 7, 7), (8, 24, 9, 13)])
 @pytest.mark.parametrize("mode", ["plain", "relu", "relu_res"])
 def test_k5_cooperative_path_matches_three_kernel_path(cuda, shape, mode, monkeypatch):
-    """Layers <= 64 MB run as ONE cooperative kernel per direction; it must agree with the
+    """Small layers run as ONE cooperative kernel per direction; it must agree with the
     three-kernel (reduce / finalize / apply) path to fp32 reduction-order noise."""
     relu, use_res = mode != "plain", mode == "relu_res"
     x, res, dy, w, b = _data(cuda, shape, torch.bfloat16, seed=21)
     res = res if use_res else None
+    monkeypatch.setenv("MBS_K5_FUSED_MB", "64")      # every case here takes the cooperative path when enabled
     monkeypatch.setenv("MBS_K5_FUSED", "1")
     a = _run(x, res, dy, w, b, relu)
     monkeypatch.setenv("MBS_K5_FUSED", "0")
