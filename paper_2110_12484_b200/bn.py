@@ -28,6 +28,7 @@ plain inference normalisation (torch ops), outside the MBS training path.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 import torch.nn.functional as F
@@ -52,6 +53,18 @@ def _workspace(rows: int, C: int, code: int, device) -> torch.Tensor:
         _native.check(_native.lib().mbs_bn_workspace_bytes(rows, C, code, ctypes.byref(out)), "mbs_bn_workspace_bytes")
         nbytes = _WS_CACHE[key] = out.value
     return torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+def _n_kernels(C: int, tensors, nbytes: int) -> int:
+    """Kernels one K5 call launches (mirrors mbs_bn.cu): 1 on the cooperative path for layers
+    <= MBS_K5_FUSED_MB (default 8 MB) with 16-byte channel vectors, else 3. Used for launch counts."""
+    v = 16 // tensors[0].element_size()
+    if os.environ.get("MBS_K5_FUSED", "1") == "0" or C % v or C // v > 256:
+        return 3
+    if any(t is not None and t.data_ptr() % 16 for t in tensors):
+        return 3
+    limit = int(os.environ.get("MBS_K5_FUSED_MB", "8")) << 20
+    return 1 if nbytes <= limit else 3
 
 
 def _channels_last(t: torch.Tensor) -> torch.Tensor:
@@ -91,7 +104,7 @@ class _MicroBatchNormFn(torch.autograd.Function):
         ws = _workspace(rows, C, code, x.device)
         stream = torch.cuda.current_stream(x.device)
         st = stream.cuda_stream
-        ev = TIMER.start_k5(3, stream)
+        ev = TIMER.start_k5(_n_kernels(C, (x, residual, y), x.numel() * x.element_size()), stream)
         _native.check(_native.lib().mbs_bn_forward(
             _ptr(x), _ptr(residual), _ptr(y), code, rows, C, _ptr(weight), _ptr(bias), _ptr(running_mean),
             _ptr(running_var), float(momentum), float(eps), int(relu), _ptr(mean), _ptr(invstd), _ptr(ws), st),
@@ -116,7 +129,8 @@ class _MicroBatchNormFn(torch.autograd.Function):
         ws = _workspace(rows, C, ctx.code, x.device)
         stream = torch.cuda.current_stream(x.device)
         st = stream.cuda_stream
-        ev = TIMER.start_k5(3, stream)
+        ev = TIMER.start_k5(_n_kernels(C, (x, residual, dy, dx, dres),
+                                       x.numel() * x.element_size() * (2 + ctx.has_res)), stream)
         _native.check(_native.lib().mbs_bn_backward(
             _ptr(x), _ptr(residual), _ptr(dy), _ptr(dx), _ptr(dres), ctx.code, rows, C, _ptr(weight), _ptr(bias),
             _ptr(mean), _ptr(invstd), int(ctx.relu), _ptr(dw), _ptr(db), _ptr(ws), st), "mbs_bn_backward")
