@@ -57,13 +57,13 @@ def _workspace(rows: int, C: int, code: int, device) -> torch.Tensor:
 
 def _n_kernels(C: int, tensors, nbytes: int) -> int:
     """Kernels one K5 call launches (mirrors mbs_bn.cu): 1 on the cooperative path for layers
-    <= MBS_K5_FUSED_MB (default 8 MB) with 16-byte channel vectors, else 3. Used for launch counts."""
+    <= MBS_K5_FUSED_MB (default 0: off) with 16-byte channel vectors, else 3. Used for launch counts."""
     v = 16 // tensors[0].element_size()
     if os.environ.get("MBS_K5_FUSED", "1") == "0" or C % v or C // v > 256:
         return 3
     if any(t is not None and t.data_ptr() % 16 for t in tensors):
         return 3
-    limit = int(os.environ.get("MBS_K5_FUSED_MB", "8")) << 20
+    limit = int(os.environ.get("MBS_K5_FUSED_MB", "0")) << 20
     return 1 if nbytes <= limit else 3
 
 

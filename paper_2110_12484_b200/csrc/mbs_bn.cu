@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_elemt(const T* __restrict
 // separate finalize launch per direction. Measured (profiles/r01_k5_fused_ab.txt, ResNet-50 step):
 // with PDL already hiding most launch gaps, limits of 0 / 8 / 16 MB are within 0.4 % of each other
 // and 32 / 64 MB are slower (the grid barriers and the register-path apply cost more than the
-// saved launches on mid-size layers), so only layers <= 8 MB take it. Same arithmetic as the
+// saved launches on mid-size layers), so it is off by default (MBS_K5_FUSED_MB enables it; the parity test forces it). Same arithmetic as the
 // three-kernel path; the partial grouping (grid size) may differ, so agreement is to fp32 noise.
 // ---------------------------------------------------------------------------------------------
 template <typename T, int V, bool RELU, bool RES>
@@ -849,7 +849,7 @@ static cudaError_t launch_tma(const T* X, const T* DY, const T* R, T* OUT, T* DR
 
 static bool tma_ok(int64_t C, int V) { return V > 1 && C / V <= kBnThreads; }
 
-constexpr int64_t kFusedMaxBytes = 8LL << 20;  // A/B: 0 / 8 / 16 MB within 0.4 %; larger limits were slower
+constexpr int64_t kFusedMaxBytes = 0;  // off by default: A/B 0 / 8 / 16 MB within 0.4 %, larger limits slower
 
 static int64_t fused_max_bytes() {  // A/B: MBS_K5_FUSED_MB overrides the size limit of the cooperative path
     const char* e = getenv("MBS_K5_FUSED_MB");

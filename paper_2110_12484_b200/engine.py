@@ -29,6 +29,7 @@ accumulated gradients agree to fp32 rounding (tests/test_engine_gpu.py).
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 from contextlib import nullcontext
 from dataclasses import dataclass, field
@@ -251,6 +252,30 @@ class GradientAccumulator:
         if self._covered >= len(self.layout.names):
             self._covered = 0
             self._fresh = False
+        self._pending_zero = False
+
+    def graph_grads_ok(self, grads: list) -> bool:
+        """Whether static (graph-captured) gradients can feed K1 without a re-layout."""
+        strides = self.layout.strides
+        return len(grads) == len(self._plist) and all(
+            g is not None and g.dtype is torch.float32 and (g.stride() == strides[j] or self._same_memory_order(g, j))
+            for j, g in enumerate(grads))
+
+    def add_pointer_table(self, ptrs, factor: float, *, loss: torch.Tensor | None = None,
+                          loss_factor: float | None = None, loss_weight: float = 0.0, last: bool = False,
+                          stream=None) -> None:
+        """K1 over every segment from a prebuilt device-pointer table (a captured micro step's gradients)."""
+        lp = None
+        if loss is not None:
+            lp = loss.data_ptr()
+        lf = float(factor if loss_factor is None else loss_factor)
+        t0 = TIMER.start(stream)
+        N.check(N.lib().mbs_accum_add(self._h, ptrs, 0, len(self._plist), float(factor), lp, lf, float(loss_weight),
+                                      int(bool(last)), _stream_ptr(stream)), "mbs_accum_add")
+        if t0 is not None:
+            TIMER.stop("k1_accumulate", t0, (8 if self._fresh else 12) * self.layout.n_params, stream)
+        self._fresh = False
+        self._covered = 0
         self._pending_zero = False
 
     def add_module_grads(self, factor: float, *, loss: torch.Tensor | None = None,
@@ -499,7 +524,7 @@ def _run_micro_loop(model, acc, plan, source, normalization, loss_kind, loss_fro
     ctx = torch.autocast("cuda", dtype=autocast_dtype) if autocast_dtype is not None else nullcontext()
     with weight_cast_cache(autocast_dtype):
         return _micro_loop_body(model, acc, plan, source, normalization, loss_kind, loss_from_logits,
-                                dice_smoothing, normalize_via, ctx, keep_outputs, outputs)
+                                dice_smoothing, normalize_via, ctx, keep_outputs, outputs, autocast_dtype)
 
 
 def weight_cast_cache(autocast_dtype):
@@ -519,12 +544,19 @@ def weight_cast_cache(autocast_dtype):
 
 
 def _micro_loop_body(model, acc, plan, source, normalization, loss_kind, loss_from_logits, dice_smoothing,
-                     normalize_via, ctx, keep_outputs, outputs):
+                     normalize_via, ctx, keep_outputs, outputs, autocast_dtype=None):
     k = -1
     for k, (xk, yk) in enumerate(source):
         if k >= plan.n_s_mu:
             raise AccumulatorOverflowError("source yielded more micro-batches than the plan")
         factor = normalization_factor(plan, k, normalization)
+        g = _graph_for(model, acc, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing,
+                       normalize_via, keep_outputs)
+        if g is not None:                 # CUDA-graph replay of fwd + loss + bwd; K1 outside the graph
+            loss = g.replay(xk, yk)
+            acc.add_pointer_table(g.ptrs, factor, loss=loss, loss_factor=factor, loss_weight=float(plan.sizes[k]),
+                                  last=(k == plan.n_s_mu - 1))
+            continue
         with ctx:
             out = model(xk)
             loss = compute_loss(loss_kind, out, yk, from_logits=loss_from_logits, dice_smoothing=dice_smoothing)
@@ -544,6 +576,36 @@ def _micro_loop_body(model, acc, plan, source, normalization, loss_kind, loss_fr
     if k + 1 != plan.n_s_mu:
         raise ValueError(f"source yielded {k + 1} micro-batches, plan expects {plan.n_s_mu}")
     return outputs
+
+
+CUDA_GRAPHS = os.environ.get("MBS_CUDA_GRAPHS", "1") != "0"
+_NO_GRAPH: set = set()
+
+
+def _graph_for(model, acc, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing, normalize_via,
+               keep_outputs):
+    """The captured micro step for this micro-batch shape, or None to run eagerly.
+
+    Graphs need: CUDA inputs, training mode, the factor applied by K1 (normalize_via "fused"), no
+    kept outputs, and fp32 gradients in the parameters' memory order. A model whose capture fails
+    runs eagerly from then on (the failure is kept, not retried every micro-batch)."""
+    if not (CUDA_GRAPHS and normalize_via == "fused" and not keep_outputs and model.training
+            and isinstance(xk, torch.Tensor) and xk.is_cuda and isinstance(yk, torch.Tensor) and yk.is_cuda):
+        return None
+    if id(model) in _NO_GRAPH:
+        return None
+    from . import graphs
+    try:
+        g = graphs.graph_for(model, acc._plist, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing)
+    except Exception as e:                 # noqa: BLE001 - capture limits: fall back to eager, loudly
+        import warnings
+        warnings.warn(f"CUDA-graph capture of the micro step failed ({type(e).__name__}: {e}); running eagerly")
+        _NO_GRAPH.add(id(model))
+        return None
+    if not acc.graph_grads_ok(g.grads):
+        _NO_GRAPH.add(id(model))
+        return None
+    return g
 
 
 def train_mini_batch(model: torch.nn.Module, params: ParameterSet, batch: tuple, plan: MicroBatchPlan,

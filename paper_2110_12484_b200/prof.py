@@ -28,7 +28,7 @@ class KernelTimer:
 
     def start(self, stream=None):
         self.launches += 1
-        if not self.enabled:
+        if not self.enabled or torch.cuda.is_current_stream_capturing():
             return None
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream or torch.cuda.current_stream())
@@ -37,7 +37,7 @@ class KernelTimer:
     def start_k5(self, n_launches: int, stream=None):
         """K5 calls launch ``n_launches`` kernels each; timed only when ``enabled and k5``."""
         self.launches += n_launches
-        if not (self.enabled and self.k5):
+        if not (self.enabled and self.k5) or torch.cuda.is_current_stream_capturing():
             return None
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream or torch.cuda.current_stream())
