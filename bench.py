@@ -219,8 +219,10 @@ def main():
         def make_batch(k):
             xb, yb = synthetic_data(w, k, seed=99, device=dev)
             return stage_rows(xb, xb.dtype, tuple(xb.shape[1:]), None, 0, k, staging, dev), yb
+        # probes at 4 / 8 samples and a 0.88 margin: at HBM-filling sizes the allocator's fragmentation
+        # and the size-dependent cuDNN workspaces are not covered by the 0.92 default
         budget = memory.measure_budget(model, make_batch, w.loss_kind, optimizer_kind=w.optimizer,
-                                       autocast_dtype=autocast)
+                                       autocast_dtype=autocast, probe=(4, 8), safety=0.88)
         n_mu = memory.fit_micro_batch(budget)
         n_b = max(w.mini, 4 * n_mu)          # a mini-batch that cannot fit HBM without streaming
         autosize = {"capacity_bytes": budget.capacity_bytes, "resident_bytes": budget.resident_bytes,

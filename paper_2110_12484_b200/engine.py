@@ -599,8 +599,10 @@ def _graph_for(model, acc, loss_kind, xk, yk, autocast_dtype, loss_from_logits, 
         g = graphs.graph_for(model, acc._plist, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing)
     except Exception as e:                 # noqa: BLE001 - capture limits: fall back to eager, loudly
         import warnings
-        warnings.warn(f"CUDA-graph capture of the micro step failed ({type(e).__name__}: {e}); running eagerly")
+        if not isinstance(e, MemoryError):
+            warnings.warn(f"CUDA-graph capture of the micro step failed ({type(e).__name__}: {e}); running eagerly")
         _NO_GRAPH.add(id(model))
+        torch.cuda.empty_cache()          # nothing of a failed capture may crowd the eager path
         return None
     if not acc.graph_grads_ok(g.grads):
         _NO_GRAPH.add(id(model))

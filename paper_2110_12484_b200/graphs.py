@@ -58,6 +58,9 @@ class MicroStepGraph:
 
         bufs = {k: v.detach().clone() for k, v in model.state_dict().items() if k not in dict(model.named_parameters())}
         saved_grads = [p.grad for p in plist]
+        torch.cuda.synchronize(dev)
+        torch.cuda.reset_peak_memory_stats(dev)
+        base = torch.cuda.memory_allocated(dev)
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):
@@ -74,6 +77,12 @@ class MicroStepGraph:
         for p in plist:
             p.grad = None
         torch.cuda.empty_cache()           # warm-up blocks back to the driver before the private pool grows
+        need = torch.cuda.max_memory_allocated(dev) - base
+        free = torch.cuda.mem_get_info(dev)[0]
+        if free < 1.15 * need + (1 << 30):
+            # the private pool would not fit next to the eager allocator's blocks (e.g. a micro-batch
+            # auto-sized to fill HBM): keep this shape eager
+            raise MemoryError(f"graph pool needs ~{need / 2**30:.1f} GiB, {free / 2**30:.1f} GiB free")
         from .prof import TIMER
         n0 = TIMER.launches
         self.graph = torch.cuda.CUDAGraph()
