@@ -142,7 +142,8 @@ class _JoinFn(torch.autograd.Function):
         cu = ctot - cs
         gup = torch.empty((n, cu, h, w), dtype=g.dtype, device=g.device, memory_format=torch.channels_last)
         _copy_channels(g, ctot, cs, gup, cu, 0, n * h * w, cu, None)
-        gb = gup.float().sum(dim=(0, 2, 3)) if has_bias and ctx.needs_input_grad[2] else None
+        # fp32 accumulation without materialising an fp32 copy of the slice
+        gb = gup.sum(dim=(0, 2, 3), dtype=torch.float32) if has_bias and ctx.needs_input_grad[2] else None
         return g, gup, gb, None
 
 

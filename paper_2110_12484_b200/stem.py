@@ -72,7 +72,7 @@ class _StemConvFn(torch.autograd.Function):
                 gm = torch.mm(cols.t(), dy2)
                 gw = gm[:K].reshape(k, k, c, o).permute(3, 2, 0, 1).to(weight.dtype).contiguous()
             if has_bias and ctx.needs_input_grad[2]:
-                gb = dy2.float().sum(0).to(weight.dtype)
+                gb = dy2.sum(0, dtype=torch.float32).to(weight.dtype)
             if ctx.needs_input_grad[0]:
                 gx = torch.nn.grad.conv2d_input(x.shape, weight.to(dy2.dtype), dy.to(dy2.dtype), s, p)
         return gx, gw, gb, None, None, None
