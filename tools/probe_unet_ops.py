@@ -32,10 +32,9 @@ from torch.profiler import profile, ProfilerActivity  # noqa: E402
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA], record_shapes=True) as prof:
     one()
     torch.cuda.synchronize()
-print(prof.key_averages(group_by_input_shape=True).table(sort_by="device_time_total", row_limit=40, max_name_column_width=60,
-                                                          max_shapes_column_width=80))
 for e in prof.events():
-    if e.name in ("aten::copy_", "aten::_to_copy", "aten::contiguous", "aten::add_", "aten::add") and e.device_time_total > 100:
+    if (e.name.startswith("aten::") and "conv" not in e.name and e.device_time_total > 150
+            and e.cpu_parent is not None and not e.cpu_parent.name.startswith("aten::")):
         print(f"{e.name:20s} {e.device_time_total / 1000:8.3f} ms  {str(e.input_shapes)[:150]}  "
               f"{[str(t)[:12] for t in getattr(e, 'concrete_inputs', [])][:3]}")
         parent = e.cpu_parent
