@@ -224,3 +224,35 @@ def test_nonfinite_loss_raises_and_keeps_params(cuda):
     with pytest.raises(mbs.NonFiniteError):
         stats.loss
     assert torch.equal(params.flat, before)          # the device guard skipped the step
+
+
+def test_cuda_graph_micro_step_matches_eager(cuda, monkeypatch):
+    """The captured micro step (graphs.MicroStepGraph) gives the eager result: same accumulated
+    gradients, loss, BN running statistics, step count; ragged tail -> a second graph."""
+    import copy
+    from paper_2110_12484_b200 import engine, graphs
+    from paper_2110_12484_b200.workloads import WORKLOADS, build_model
+    torch.manual_seed(0)
+    base = build_model(WORKLOADS["c1"], ops="native").to(cuda).to(memory_format=torch.channels_last)
+    g = torch.Generator().manual_seed(3)
+    x = torch.randn(20, 3, 32, 32, generator=g).to(cuda).contiguous(memory_format=torch.channels_last)
+    y = torch.randint(0, 10, (20,), generator=g).to(cuda)
+    res = {}
+    for use in (False, True):
+        monkeypatch.setattr(engine, "CUDA_GRAPHS", use)
+        graphs.clear()
+        net = copy.deepcopy(base)
+        params = mbs.ParameterSet(net)
+        for _ in range(2):                                   # second pass replays the captured graphs
+            total, st = mbs.mini_batch_gradient(net, params, x, y, mbs.plan_split(20, 8), "exact_weighted",
+                                                "cross_entropy")
+        res[use] = (np.concatenate([total[n].detach().double().cpu().numpy().ravel() for n in params.names()]),
+                    st.loss, {k: v.detach().clone() for k, v in net.state_dict().items() if "running" in k})
+        if use:
+            assert len(graphs._CACHE) == 2                  # [8, 8, 4]: full + tail shape
+    a, b = res[False], res[True]
+    assert np.linalg.norm(a[0] - b[0]) / np.linalg.norm(a[0]) <= 1e-5
+    assert abs(a[1] - b[1]) <= 1e-5 * abs(a[1])
+    for k in a[2]:
+        assert torch.allclose(a[2][k], b[2][k], rtol=1e-5, atol=1e-6), k
+    graphs.clear()
