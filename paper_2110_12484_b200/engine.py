@@ -556,6 +556,8 @@ def _micro_loop_body(model, acc, plan, source, normalization, loss_kind, loss_fr
             loss = g.replay(xk, yk)
             acc.add_pointer_table(g.ptrs, factor, loss=loss, loss_factor=factor, loss_weight=float(plan.sizes[k]),
                                   last=(k == plan.n_s_mu - 1))
+            if keep_outputs:
+                outputs.append(g.out.clone())   # the static output is overwritten by the next replay
             continue
         with ctx:
             out = model(xk)
@@ -586,10 +588,10 @@ def _graph_for(model, acc, loss_kind, xk, yk, autocast_dtype, loss_from_logits, 
                keep_outputs):
     """The captured micro step for this micro-batch shape, or None to run eagerly.
 
-    Graphs need: CUDA inputs, training mode, the factor applied by K1 (normalize_via "fused"), no
-    kept outputs, and fp32 gradients in the parameters' memory order. A model whose capture fails
+    Graphs need: CUDA inputs, training mode, the factor applied by K1 (normalize_via "fused") and
+    fp32 gradients in the parameters' memory order (kept outputs are cloned from the static output). A model whose capture fails
     runs eagerly from then on (the failure is kept, not retried every micro-batch)."""
-    if not (CUDA_GRAPHS and normalize_via == "fused" and not keep_outputs and model.training
+    if not (CUDA_GRAPHS and normalize_via == "fused" and model.training
             and isinstance(xk, torch.Tensor) and xk.is_cuda and isinstance(yk, torch.Tensor) and yk.is_cuda):
         return None
     if id(model) in _NO_GRAPH:

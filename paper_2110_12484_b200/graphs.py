@@ -54,7 +54,7 @@ class MicroStepGraph:
                 loss = compute_loss(loss_kind, out, self.y, from_logits=loss_from_logits,
                                     dice_smoothing=dice_smoothing)
             loss.backward()
-            return loss
+            return loss, out
 
         bufs = {k: v.detach().clone() for k, v in model.state_dict().items() if k not in dict(model.named_parameters())}
         saved_grads = [p.grad for p in plist]
@@ -87,7 +87,8 @@ class MicroStepGraph:
         n0 = TIMER.launches
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.loss = step().detach()
+            loss, out = step()
+            self.loss, self.out = loss.detach(), out.detach()
         self.native_launches = TIMER.launches - n0   # this repo's kernels inside the graph (K5/K6/K7/...)
         self.grads = [p.grad for p in plist]
         if any(g is None for g in self.grads):
