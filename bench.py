@@ -295,22 +295,24 @@ def main():
             ms = float(t.item())
         return ms, losses
 
-    # --- value: inputs resident in HBM ---
+    # --- value: inputs resident in HBM (no per-kernel instrumentation inside the timed region) ---
     with ClockSampler(dev.index) as clocks:
-        ms_dev, _ = timed(False, args.steps, args.warmup, k1_timer=True)
-    kstats = TIMER.summary()
+        ms_dev, _ = timed(False, args.steps, args.warmup, k1_timer=False)
     launches_value = TIMER.launches
-    # K5 (model BatchNorm) bandwidth: one more HBM-resident mini-batch with its launches timed (not in `value`)
-    k5stats = {}
-    if args.model_ops == "native":
-        from paper_2110_12484_b200 import engine as _eng
-        graphs_on, _eng.CUDA_GRAPHS = _eng.CUDA_GRAPHS, False   # K5 calls are timed one by one: eager
-        TIMER.reset()
-        TIMER.enabled = TIMER.k5 = True
-        epoch(False, 1, 2000, warm_mini)
-        TIMER.enabled = TIMER.k5 = False
-        _eng.CUDA_GRAPHS = graphs_on
-        k5stats = {k: v for k, v in TIMER.summary().items() if k.startswith("k5_")}
+    # Per-kernel bandwidths (K1 accumulate, K2, K3, K4 and the model's K5 BatchNorm): two more
+    # HBM-resident mini-batches, eager, with CUDA events around every launch on its stream. Kept out of
+    # `value` so the events and the eager launches do not perturb the headline number.
+    from paper_2110_12484_b200 import engine as _eng
+    graphs_on, _eng.CUDA_GRAPHS = _eng.CUDA_GRAPHS, False
+    TIMER.reset()
+    TIMER.enabled = True
+    TIMER.k5 = args.model_ops == "native"
+    epoch(False, 2, 2000, warm_mini)
+    TIMER.enabled = TIMER.k5 = False
+    _eng.CUDA_GRAPHS = graphs_on
+    allstats = TIMER.summary()
+    kstats = {k: v for k, v in allstats.items() if not k.startswith("k5_")}
+    k5stats = {k: v for k, v in allstats.items() if k.startswith("k5_")}
     samples_total = n_b * args.steps * ws
     value = samples_total / (ms_dev / 1e3)
 
@@ -370,6 +372,8 @@ def main():
                 "launches_timed": k1.get("launches"),
                 "bytes_rule": "12 B/param (read g, read acc, write acc); 8 B/param on the first micro-batch "
                               "(acc = s*g); P = %d" % params.layout.n_params,
+                "how": "CUDA events around every K1 launch of two extra HBM-resident mini-batches (eager), "
+                       "outside the timed region",
                 "other_kernels": {k: {"gbs": v["gbs"], "avg_us": v["avg_ms"] * 1e3, "launches": v["launches"]}
                                   for k, v in kstats.items() if k != "k1_accumulate"}}
     try:
