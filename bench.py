@@ -443,10 +443,13 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch"):
+def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True):
     """The paper's 'w/o MBS' run: plain torch training, batch = micro-batch, data resident in HBM.
 
-    ``ops`` selects the same model definition as the MBS run (native K5/K6 or stock torch ops)."""
+    ``ops`` selects the same model definition as the MBS run (native K5/K6/K7 or stock torch ops).
+    ``graph``: the whole training step (fwd + bwd + fused optimizer step) is replayed from one CUDA
+    graph, like the MBS micro step — eager, this loop is host-bound on B200 and its number then
+    tracks the host CPU rather than the GPU. Falls back to eager if capture fails."""
     from paper_2110_12484_b200.losses import compute_loss
     from paper_2110_12484_b200.workloads import build_model, synthetic_data
     torch.manual_seed(0)
@@ -454,22 +457,53 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch"):
     if w.optimizer == "sgd":
         opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9, weight_decay=5e-4, fused=True)
     else:
-        opt = torch.optim.Adam(model.parameters(), lr=0.01, weight_decay=5e-4, fused=True)
+        opt = torch.optim.Adam(model.parameters(), lr=0.01, weight_decay=5e-4, fused=True, capturable=graph)
     x, y = synthetic_data(w, 2 * batch, seed=7, device=dev)
     xs = [x[i * batch:(i + 1) * batch].to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
           for i in range(2)]
     ys = [y[i * batch:(i + 1) * batch] for i in range(2)]
+    sx, sy = xs[0].clone(), ys[0].clone()
 
-    def one(i):
-        with torch.autocast("cuda", dtype=torch.bfloat16):
-            loss = compute_loss(w.loss_kind, model(xs[i % 2]), ys[i % 2])
+    def step(cache=True):
+        with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=cache):
+            loss = compute_loss(w.loss_kind, model(sx), sy)
         loss.backward()
         opt.step()
-        opt.zero_grad(set_to_none=True)
         return loss
+
+    def one(i):
+        sx.copy_(xs[i % 2])
+        sy.copy_(ys[i % 2])
+        step()
+        opt.zero_grad(set_to_none=True)
 
     for i in range(warmup):
         one(i)
+    torch.cuda.synchronize(dev)
+    how = "torch fwd/bwd + fused torch.optim step per batch, bf16 autocast, data in HBM"
+    if graph:
+        try:
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                for i in range(2):
+                    one(i)
+            torch.cuda.current_stream(dev).wait_stream(side)
+            torch.cuda.synchronize(dev)
+            opt.zero_grad(set_to_none=True)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step(cache=False)
+
+            def one(i):                                  # noqa: F811 - the graphed step
+                sx.copy_(xs[i % 2])
+                sy.copy_(ys[i % 2])
+                g.replay()
+            for i in range(2):
+                one(i)
+            how = "CUDA graph of torch fwd/bwd + fused torch.optim step per batch, bf16 autocast, data in HBM"
+        except Exception as e:                           # noqa: BLE001
+            print(f"no-stream baseline: graph capture failed ({type(e).__name__}: {e}); eager", file=sys.stderr)
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n = steps * max(1, w.mini // batch)
@@ -481,8 +515,7 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch"):
     ms = e0.elapsed_time(e1)
     del model, opt
     return {"value": batch * n * ws / (ms / 1e3), "unit": "samples/s", "batch": batch,
-            "steps": n, "model_ops": ops,
-            "how": "torch fwd/bwd + fused torch.optim step per batch, bf16 autocast, data in HBM"}
+            "steps": n, "model_ops": ops, "how": how}
 
 
 if __name__ == "__main__":
