@@ -206,7 +206,7 @@ def main():
     torch.manual_seed(1234 + rank)
 
     model = build_model(w, ops=args.model_ops).to(dev).to(memory_format=torch.channels_last)
-    params = mbs.ParameterSet(model)
+    params = mbs.ParameterSet(model, shadow=torch.bfloat16)   # bf16 shadow weights: K3 refreshes them, K1 reads bf16 grads
     staging = Staging(dtype=torch.bfloat16, channels_last=True)
     autocast = torch.bfloat16
     n_b, n_mu = w.mini, w.micro

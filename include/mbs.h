@@ -101,6 +101,12 @@ int mbs_accum_zero(mbs_accum_t h, void* stream);
 int mbs_accum_add(mbs_accum_t h, const float* const* grads, int64_t seg_begin,
                   int64_t seg_count, double factor, const float* loss_dev,
                   double loss_factor, double loss_weight, int last, void* stream);
+/* Same, with a per-segment gradient dtype: dtypes[i] is MBS_F32 or MBS_BF16 (NULL: all fp32). bf16
+ * gradients (the weight gradients of a bf16 shadow-weight forward) are widened exactly in K1, so no
+ * fp32 conversion pass is needed before accumulation. */
+int mbs_accum_add_typed(mbs_accum_t h, const void* const* grads, const int* dtypes, int64_t seg_begin,
+                        int64_t seg_count, double factor, const float* loss_dev, double loss_factor,
+                        double loss_weight, int last, void* stream);
 /* Same, over a flat gradient buffer laid out exactly like acc. */
 int mbs_accum_add_flat(mbs_accum_t h, const float* g_flat, double factor,
                        const float* loss_dev, double loss_factor, double loss_weight, int last,
@@ -124,12 +130,17 @@ int mbs_accum_seen(mbs_accum_t h, int64_t* seen, int64_t* expected);
  * intact, the host raises NonFiniteError when it reads the stats).
  * `velocity`/`m`/`v` are device fp32 buffers of `numel` elements, zero at
  * step 0 (the reference creates them lazily as zeros, optim.py:58-61,78-83).
+ * `shadow_bf16` (nullable, 8-byte aligned, numel bf16 values) receives the
+ * round-to-nearest-even bf16 copy of the updated weights in the same pass —
+ * the weights the next mini-batch's bf16 forward reads (shadow-weight mode).
  * ------------------------------------------------------------------------- */
 int mbs_sgd_step(float* w, const float* grad, float* velocity, int64_t numel, double lr,
-                 double momentum, double weight_decay, const double* guard_dev, void* stream);
+                 double momentum, double weight_decay, const double* guard_dev, void* shadow_bf16,
+                 void* stream);
 int mbs_adam_step(float* w, const float* grad, float* m, float* v, int64_t numel, double lr,
                   double beta1, double beta2, double eps, double weight_decay,
-                  int64_t step /* t = step_count + 1 */, const double* guard_dev, void* stream);
+                  int64_t step /* t = step_count + 1 */, const double* guard_dev, void* shadow_bf16,
+                  void* stream);
 
 /* ---------------------------------------------------------------------------
  * Staging — engine.py:310-311 (x[order[mini]]) + engine.py:149-151

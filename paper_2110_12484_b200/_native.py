@@ -46,14 +46,16 @@ _SIGS = {
     "mbs_accum_zero": (c_int, [c_void_p, c_void_p]),
     "mbs_accum_add": (c_int, [c_void_p, POINTER(c_void_p), c_int64, c_int64, c_double, c_void_p, c_double, c_double,
                               c_int, c_void_p]),
+    "mbs_accum_add_typed": (c_int, [c_void_p, POINTER(c_void_p), c_void_p, c_int64, c_int64, c_double, c_void_p,
+                                    c_double, c_double, c_int, c_void_p]),
     "mbs_accum_add_flat": (c_int, [c_void_p, c_void_p, c_double, c_void_p, c_double, c_double, c_int, c_void_p]),
     "mbs_accum_norm": (c_int, [c_void_p, c_void_p]),
     "mbs_accum_finalize": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
     "mbs_accum_seen": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64)]),
     "mbs_sgd_step": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_double, c_double, c_double, c_void_p,
-                             c_void_p]),
+                             c_void_p, c_void_p]),
     "mbs_adam_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_double, c_double, c_double,
-                              c_double, c_double, c_int64, c_void_p, c_void_p]),
+                              c_double, c_double, c_int64, c_void_p, c_void_p, c_void_p]),
     "mbs_stage": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p, c_int,
                           c_int, c_void_p]),
     "mbs_gather_rows": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]),

@@ -12,6 +12,7 @@
 // independent float4s in flight per thread, one CTA per 8192-element chunk
 // (the hardware block scheduler balances the tail), no atomics, and a fixed
 // reduction order so the grad norm is bit-reproducible run to run.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdlib.h>
@@ -79,6 +80,23 @@ __device__ __forceinline__ double sq4(float4 a) {
     return x * x + y * y + z * z + w * w;
 }
 
+// bf16 gradients (the shadow-weight path: cuDNN's weight gradients stay bf16, no conversion pass):
+// 4 elements per 8-byte streaming load, widened exactly to fp32.
+__device__ __forceinline__ float4 ld_stream_bf16x4(const uint2* p) {
+    uint32_t a, b;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
+    return make_float4(__uint_as_float(a << 16), __uint_as_float(a & 0xffff0000u), __uint_as_float(b << 16),
+                       __uint_as_float(b & 0xffff0000u));
+}
+
+__device__ __forceinline__ float bf16_to_f32(const __nv_bfloat16 v) { return __bfloat162float(v); }
+
+// round-to-nearest-even fp32 -> bf16 of 4 values packed for one 8-byte store (torch's .to(bfloat16))
+__device__ __forceinline__ uint2 pack_bf16x4(const float4 v) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    return make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+}
+
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* smem) {
 #pragma unroll
@@ -106,13 +124,13 @@ __device__ __forceinline__ int find_seg(const Seg* __restrict__ segs, int s0, in
 
 // One contiguous piece of one segment: acc[0..n) (+)= s * g[0..n). Pieces never exceed one CTA
 // share (<= 2^31 elements), so the inner loops use 32-bit indices (keeps K1 at ~56 registers).
-template <bool ASSIGN, bool NORM>
-__device__ __forceinline__ void accum_piece(float* __restrict__ a, const float* __restrict__ g, int n, float s,
+template <bool ASSIGN, bool NORM, typename G>
+__device__ __forceinline__ void accum_piece(float* __restrict__ a, const G* __restrict__ g, int n, float s,
                                             double& sq) {
+    constexpr int kAlign = sizeof(G) == 4 ? 15 : 7;   // 16-byte float4 / 8-byte bf16x4 loads
     int done = 0;
-    if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+    if ((reinterpret_cast<uintptr_t>(g) & kAlign) == 0) {
         const int n4 = n >> 2;
-        const float4* g4 = reinterpret_cast<const float4*>(g);
         float4* a4 = reinterpret_cast<float4*>(a);
         for (int base = threadIdx.x; base < n4; base += kThreads * kUnroll) {
             float4 gv[kUnroll], av[kUnroll];
@@ -120,7 +138,10 @@ __device__ __forceinline__ void accum_piece(float* __restrict__ a, const float* 
             for (int u = 0; u < kUnroll; ++u) {
                 const int i = base + u * kThreads;
                 if (i < n4) {
-                    gv[u] = ld_stream(g4 + i);
+                    if constexpr (sizeof(G) == 4)
+                        gv[u] = ld_stream(reinterpret_cast<const float4*>(g) + i);
+                    else
+                        gv[u] = ld_stream_bf16x4(reinterpret_cast<const uint2*>(g) + i);
                     if (!ASSIGN) av[u] = ld_acc(a4 + i);
                 }
             }
@@ -143,15 +164,13 @@ __device__ __forceinline__ void accum_piece(float* __restrict__ a, const float* 
         done = n4 << 2;
     }
     for (int i = done + threadIdx.x; i < n; i += kThreads) {  // tail / unaligned gradient
-        const float r = ASSIGN ? s * g[i] : fmaf(s, g[i], a[i]);
+        float gi;
+        if constexpr (sizeof(G) == 4) gi = g[i]; else gi = bf16_to_f32(g[i]);
+        const float r = ASSIGN ? s * gi : fmaf(s, gi, a[i]);
         a[i] = r;
         if (NORM) sq += (double)r * (double)r;
     }
 }
-
-// K1: CTA b owns acc elements [lo0 + b*per_block, +per_block) — a balanced, 128-byte aligned share
-// of the launch's range that may span several segments (small BN/bias tensors) or part of one.
-// acc = s*g (ASSIGN) or acc += s*g; NORM adds this CTA's sum of squares to partials[b].
 template <bool ASSIGN, bool NORM>
 __global__ void __launch_bounds__(kThreads, MBS_K1_MINBLOCKS)
 k_accum(float* __restrict__ acc, const Seg* __restrict__ segs, const int* __restrict__ tile_seg, int seg0, int seg1,
@@ -171,7 +190,15 @@ k_accum(float* __restrict__ acc, const Seg* __restrict__ segs, const int* __rest
             const Seg sg = segs[si];
             if (sg.off >= hi) break;
             const int64_t p0 = max(lo, sg.off), p1 = min(hi, sg.off + sg.num);
-            if (p1 > p0) accum_piece<ASSIGN, NORM>(acc + p0, gp.p[si - seg0] + (p0 - sg.off), (int)(p1 - p0), s, sq);
+            if (p1 <= p0) continue;
+            // bit 0 of a gradient pointer tags bf16 data (bf16 is 2-byte aligned, fp32 4-byte)
+            const uintptr_t raw = reinterpret_cast<uintptr_t>(gp.p[si - seg0]);
+            if (raw & 1)
+                accum_piece<ASSIGN, NORM>(acc + p0, reinterpret_cast<const __nv_bfloat16*>(raw & ~(uintptr_t)1) +
+                                                        (p0 - sg.off), (int)(p1 - p0), s, sq);
+            else
+                accum_piece<ASSIGN, NORM>(acc + p0, reinterpret_cast<const float*>(raw) + (p0 - sg.off),
+                                          (int)(p1 - p0), s, sq);
         }
     }
     if (NORM) {
@@ -257,7 +284,7 @@ __device__ __forceinline__ void sgd4(float4& ww, float4& vv, const float4 gg, fl
 template <bool READ_V, bool WD>
 __global__ void __launch_bounds__(kThreads)
 k_sgd(float4* __restrict__ w, const float4* __restrict__ g, float4* __restrict__ v, int64_t n4,
-      float lr, float mu, float wd, const double* __restrict__ guard) {
+      float lr, float mu, float wd, const double* __restrict__ guard, uint2* __restrict__ shadow) {
     if (guard_tripped(guard)) return;
     constexpr int U = MBS_K3_UNROLL;
     const int64_t stride = (int64_t)gridDim.x * kThreads;
@@ -279,6 +306,7 @@ k_sgd(float4* __restrict__ w, const float4* __restrict__ g, float4* __restrict__
                 sgd4<READ_V, WD>(ww[u], vv[u], gg[u], lr, mu, wd);
                 v[j] = vv[u];
                 w[j] = ww[u];
+                if (shadow) shadow[j] = pack_bf16x4(ww[u]);   // the bf16 weights the next forward reads
             }
         }
     }
@@ -307,7 +335,7 @@ __device__ __forceinline__ void adam4(float4& ww, float4& mm, float4& vv, const 
 __global__ void __launch_bounds__(kThreads)
 k_adam(float4* __restrict__ w, const float4* __restrict__ g, float4* __restrict__ m,
        float4* __restrict__ v, int64_t n4, float lr, float b1, float b2, float omb1, float omb2, float c1, float c2,
-       float eps, float wd, const double* __restrict__ guard) {
+       float eps, float wd, const double* __restrict__ guard, uint2* __restrict__ shadow) {
     // omb = 1 - beta is formed in double on the host: 1.f - 0.999f carries a 1.3e-5 relative error
     if (guard_tripped(guard)) return;
     const int64_t stride = (int64_t)gridDim.x * kThreads;
@@ -323,9 +351,11 @@ k_adam(float4* __restrict__ w, const float4* __restrict__ g, float4* __restrict_
         }
         adam4(w0, m0, v0, g0, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
         w[i] = w0; m[i] = m0; v[i] = v0;
+        if (shadow) shadow[i] = pack_bf16x4(w0);
         if (two) {
             adam4(w1, m1, v1, g1, lr, b1, omb1, b2, omb2, c1, c2, eps, wd);
             w[i2] = w1; m[i2] = m1; v[i2] = v1;
+            if (shadow) shadow[i2] = pack_bf16x4(w1);
         }
     }
 }
@@ -551,9 +581,9 @@ static int64_t share(int64_t range, int grid, int64_t tile) {
     return (per + 31) / 32 * 32;
 }
 
-static int launch_accum(mbs_accum_t h, const float* const* grads, int64_t seg_begin, int64_t seg_count,
-                        float s, const float* loss_dev, double factor, double weight, bool assign, bool norm,
-                        cudaStream_t st) {
+static int launch_accum(mbs_accum_t h, const void* const* grads, const int* dtypes, int64_t seg_begin,
+                        int64_t seg_count, float s, const float* loss_dev, double factor, double weight, bool assign,
+                        bool norm, cudaStream_t st) {
     const int64_t slot = h->seen;
     const int64_t nseg = (int64_t)h->off.size();
     // the norm partials are only meaningful for a launch covering every segment
@@ -561,7 +591,10 @@ static int launch_accum(mbs_accum_t h, const float* const* grads, int64_t seg_be
     for (int64_t b = 0; b < seg_count; b += kMaxPtrs) {
         const int64_t cnt = std::min<int64_t>(kMaxPtrs, seg_count - b);
         GradPtrs gp;
-        for (int64_t i = 0; i < cnt; ++i) gp.p[i] = grads[b + i];
+        for (int64_t i = 0; i < cnt; ++i) {
+            const bool bf = dtypes != nullptr && dtypes[b + i] == MBS_BF16;
+            gp.p[i] = reinterpret_cast<const float*>(reinterpret_cast<uintptr_t>(grads[b + i]) | (bf ? 1u : 0u));
+        }
         const int s0 = (int)(seg_begin + b), s1 = (int)(seg_begin + b + cnt);
         const int64_t lo = h->off[s0], hi = h->off[s1 - 1] + h->num[s1 - 1];
         if (hi <= lo) continue;
@@ -586,10 +619,16 @@ static int launch_accum(mbs_accum_t h, const float* const* grads, int64_t seg_be
     return MBS_OK;
 }
 
-int mbs_accum_add(mbs_accum_t h, const float* const* grads, int64_t seg_begin, int64_t seg_count,
-                  double factor, const float* loss_dev, double loss_factor, double loss_weight, int last,
-                  void* stream) {
+int mbs_accum_add_typed(mbs_accum_t h, const void* const* grads, const int* dtypes, int64_t seg_begin,
+                        int64_t seg_count, double factor, const float* loss_dev, double loss_factor,
+                        double loss_weight, int last, void* stream) {
     if (!h || !grads) return invalid("null accumulator or gradient table");
+    if (dtypes)
+        for (int64_t i = 0; i < seg_count; ++i) {
+            if (dtypes[i] != MBS_F32 && dtypes[i] != MBS_BF16) return invalid("gradient dtype must be f32 or bf16");
+            if (dtypes[i] == MBS_BF16 && (reinterpret_cast<uintptr_t>(grads[i]) & 1))
+                return invalid("bf16 gradient pointer not 2-byte aligned");
+        }
     const int64_t nseg = (int64_t)h->off.size();
     if (seg_begin < 0 || seg_count < 1 || seg_begin + seg_count > nseg)
         return invalid("segment range out of bounds");
@@ -616,8 +655,8 @@ int mbs_accum_add(mbs_accum_t h, const float* const* grads, int64_t seg_begin, i
             set_error("missing gradient for segment " + std::to_string(seg_begin + i));
             return MBS_EKEY;
         }
-    int st = launch_accum(h, grads, seg_begin, seg_count, (float)factor, loss_dev, loss_factor, loss_weight, h->fresh,
-                          last != 0, (cudaStream_t)stream);
+    int st = launch_accum(h, grads, dtypes, seg_begin, seg_count, (float)factor, loss_dev, loss_factor, loss_weight,
+                          h->fresh, last != 0, (cudaStream_t)stream);
     if (st) return st;
     h->covered += seg_count;
     if (h->covered == nseg) {
@@ -626,6 +665,13 @@ int mbs_accum_add(mbs_accum_t h, const float* const* grads, int64_t seg_begin, i
         h->fresh = false;
     }
     return MBS_OK;
+}
+
+int mbs_accum_add(mbs_accum_t h, const float* const* grads, int64_t seg_begin, int64_t seg_count,
+                  double factor, const float* loss_dev, double loss_factor, double loss_weight, int last,
+                  void* stream) {
+    return mbs_accum_add_typed(h, reinterpret_cast<const void* const*>(grads), nullptr, seg_begin, seg_count, factor,
+                               loss_dev, loss_factor, loss_weight, last, stream);
 }
 
 int mbs_accum_add_flat(mbs_accum_t h, const float* g_flat, double factor, const float* loss_dev,
@@ -660,7 +706,9 @@ int mbs_accum_finalize(mbs_accum_t h, int64_t n_b, double* stats_dev, void* stre
 }
 
 int mbs_sgd_step(float* w, const float* grad, float* velocity, int64_t numel, double lr, double momentum,
-                 double weight_decay, const double* guard_dev, void* stream) {
+                 double weight_decay, const double* guard_dev, void* shadow_bf16, void* stream) {
+    if (shadow_bf16 && ((uintptr_t)shadow_bf16 & 7)) return invalid("mbs_sgd_step: shadow must be 8-byte aligned");
+    auto SH = reinterpret_cast<uint2*>(shadow_bf16);
     if (!w || !grad || !velocity || numel <= 0 || numel % 4)
         return invalid("mbs_sgd_step: null buffer or numel not a positive multiple of 4");
     if (((uintptr_t)w | (uintptr_t)grad | (uintptr_t)velocity) & 15) return invalid("mbs_sgd_step: buffers must be 16-byte aligned");
@@ -671,17 +719,18 @@ int mbs_sgd_step(float* w, const float* grad, float* velocity, int64_t numel, do
     auto G = reinterpret_cast<const float4*>(grad);
     auto V = reinterpret_cast<float4*>(velocity);
     const bool rv = momentum != 0.0, wd = weight_decay != 0.0;
-    if (rv && wd) k_sgd<true, true><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, (float)momentum, (float)weight_decay, guard_dev);
-    else if (rv) k_sgd<true, false><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, (float)momentum, 0.f, guard_dev);
-    else if (wd) k_sgd<false, true><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, 0.f, (float)weight_decay, guard_dev);
-    else k_sgd<false, false><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, 0.f, 0.f, guard_dev);
+    if (rv && wd) k_sgd<true, true><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, (float)momentum, (float)weight_decay, guard_dev, SH);
+    else if (rv) k_sgd<true, false><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, (float)momentum, 0.f, guard_dev, SH);
+    else if (wd) k_sgd<false, true><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, 0.f, (float)weight_decay, guard_dev, SH);
+    else k_sgd<false, false><<<grid, kThreads, 0, st>>>(W, G, V, n4, (float)lr, 0.f, 0.f, guard_dev, SH);
     MBS_CK_LAUNCH("k_sgd");
     return MBS_OK;
 }
 
 int mbs_adam_step(float* w, const float* grad, float* m, float* v, int64_t numel, double lr, double beta1,
                   double beta2, double eps, double weight_decay, int64_t step, const double* guard_dev,
-                  void* stream) {
+                  void* shadow_bf16, void* stream) {
+    if (shadow_bf16 && ((uintptr_t)shadow_bf16 & 7)) return invalid("mbs_adam_step: shadow must be 8-byte aligned");
     if (!w || !grad || !m || !v || numel <= 0 || numel % 4 || step < 1)
         return invalid("mbs_adam_step: null buffer, numel not a positive multiple of 4, or step < 1");
     if (((uintptr_t)w | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v) & 15) return invalid("mbs_adam_step: buffers must be 16-byte aligned");
@@ -691,7 +740,7 @@ int mbs_adam_step(float* w, const float* grad, float* m, float* v, int64_t numel
         reinterpret_cast<float4*>(w), reinterpret_cast<const float4*>(grad), reinterpret_cast<float4*>(m),
         reinterpret_cast<float4*>(v), n4, (float)lr, (float)beta1, (float)beta2, (float)(1.0 - beta1),
         (float)(1.0 - beta2), (float)c1, (float)c2, (float)eps,
-        (float)weight_decay, guard_dev);
+        (float)weight_decay, guard_dev, reinterpret_cast<uint2*>(shadow_bf16));
     MBS_CK_LAUNCH("k_adam");
     return MBS_OK;
 }

@@ -141,8 +141,17 @@ class GradientAccumulator:
                                          self.max_micro, ctypes.byref(h)), "mbs_accum_create")
         self._h = h
         self._views = self.layout.views(self.flat)
-        self._plist = [params[n] for n in self.layout.names]
+        # the tensors autograd fills: the module's parameters (bf16 shadows in shadow-weight mode)
+        self._plist = list(params.grad_params) if params.grad_params is not None else \
+            [params[n] for n in self.layout.names]
         self._ptr_table = (ctypes.c_void_p * len(self._plist))()
+        self._dtype_table = (ctypes.c_int * len(self._plist))(
+            *[N.BF16 if p.dtype == torch.bfloat16 else N.F32 for p in self._plist])
+        self._typed = any(p.dtype == torch.bfloat16 for p in self._plist)
+        gsz = [2 if p.dtype == torch.bfloat16 else 4 for p in self._plist]
+        # algorithmic K1 bytes per full pass: read g (2 or 4 B) + write acc (4 B) [+ read acc (4 B)]
+        self._k1_bytes_assign = sum(n * (g + 4) for n, g in zip(self.layout.numels, gsz))
+        self._k1_bytes_acc = self._k1_bytes_assign + 4 * self.layout.n_params
         self._pending_zero = False
         self._fresh = True
         self._covered = 0
@@ -214,14 +223,25 @@ class GradientAccumulator:
             return False
         return sum((n - 1) * st for n, st in zip(shape, g.stride())) == g.numel() - 1   # dense, no overlap
 
-    def _conform(self, g: torch.Tensor, i: int) -> torch.Tensor:
+    def _conform(self, g: torch.Tensor, i: int, allow_bf16: bool = True) -> torch.Tensor:
+        """g in the segment's memory order and in fp32 or bf16 (K1 reads both; anything else is cast;
+        ``allow_bf16=False`` for the fp32-only peer all-reduce kernel)."""
         shape, stride = self.layout.shapes[i], self.layout.strides[i]
-        if g.dtype == torch.float32 and g.device == self.flat.device and (
+        ok = (torch.float32, torch.bfloat16) if allow_bf16 else (torch.float32,)
+        if g.dtype in ok and g.device == self.flat.device and (
                 tuple(g.stride()) == stride or self._same_memory_order(g, i)):
             return g
         out = torch.empty_strided(shape, stride, dtype=torch.float32, device=self.flat.device)
         out.copy_(g)
         return out
+
+    def _add(self, ptrs, dtypes, seg_begin, n, factor, lp, lf, loss_weight, last, stream):
+        if dtypes is None:
+            return N.lib().mbs_accum_add(self._h, ptrs, seg_begin, n, float(factor), lp, lf, float(loss_weight),
+                                         int(bool(last)), _stream_ptr(stream))
+        return N.lib().mbs_accum_add_typed(self._h, ptrs, ctypes.cast(dtypes, ctypes.c_void_p), seg_begin, n,
+                                           float(factor), lp, lf, float(loss_weight), int(bool(last)),
+                                           _stream_ptr(stream))
 
     def add_tensors(self, tensors: list, factor: float, *, loss: torch.Tensor | None = None,
                     loss_factor: float | None = None, loss_weight: float = 0.0, last: bool = False,
@@ -229,11 +249,13 @@ class GradientAccumulator:
         """K1 over segments [seg_begin, seg_begin+len(tensors)): acc (+)= factor * g."""
         n = len(tensors)
         ptrs = (ctypes.c_void_p * n)()
+        dtypes = (ctypes.c_int * n)()
         keep = []
         for j, g in enumerate(tensors):
             g = self._conform(g, seg_begin + j)
             keep.append(g)
             ptrs[j] = g.data_ptr()
+            dtypes[j] = N.BF16 if g.dtype == torch.bfloat16 else N.F32
         lp = None
         if loss is not None:
             loss = loss.detach()
@@ -243,11 +265,11 @@ class GradientAccumulator:
             lp = loss.data_ptr()
         lf = float(factor if loss_factor is None else loss_factor)
         t0 = TIMER.start(stream)
-        N.check(N.lib().mbs_accum_add(self._h, ptrs, int(seg_begin), n, float(factor), lp, lf, float(loss_weight),
-                                      int(bool(last)), _stream_ptr(stream)), "mbs_accum_add")
+        N.check(self._add(ptrs, dtypes, int(seg_begin), n, factor, lp, lf, loss_weight, last, stream), "mbs_accum_add")
         if t0 is not None:
+            nb = sum((2 if t.dtype == torch.bfloat16 else 4) * t.numel() for t in keep[:n])
             elems = sum(self.layout.numels[seg_begin:seg_begin + n])
-            TIMER.stop("k1_accumulate", t0, (8 if self._fresh else 12) * elems, stream)
+            TIMER.stop("k1_accumulate", t0, nb + (4 if self._fresh else 8) * elems, stream)
         self._covered += n
         if self._covered >= len(self.layout.names):
             self._covered = 0
@@ -258,8 +280,8 @@ class GradientAccumulator:
         """Whether static (graph-captured) gradients can feed K1 without a re-layout."""
         strides = self.layout.strides
         return len(grads) == len(self._plist) and all(
-            g is not None and g.dtype is torch.float32 and (g.stride() == strides[j] or self._same_memory_order(g, j))
-            for j, g in enumerate(grads))
+            g is not None and g.dtype is p.dtype and (g.stride() == strides[j] or self._same_memory_order(g, j))
+            for j, (g, p) in enumerate(zip(grads, self._plist)))
 
     def add_pointer_table(self, ptrs, factor: float, *, loss: torch.Tensor | None = None,
                           loss_factor: float | None = None, loss_weight: float = 0.0, last: bool = False,
@@ -270,10 +292,10 @@ class GradientAccumulator:
             lp = loss.data_ptr()
         lf = float(factor if loss_factor is None else loss_factor)
         t0 = TIMER.start(stream)
-        N.check(N.lib().mbs_accum_add(self._h, ptrs, 0, len(self._plist), float(factor), lp, lf, float(loss_weight),
-                                      int(bool(last)), _stream_ptr(stream)), "mbs_accum_add")
+        N.check(self._add(ptrs, self._dtype_table, 0, len(self._plist), factor, lp, lf, loss_weight, last, stream),
+                "mbs_accum_add")
         if t0 is not None:
-            TIMER.stop("k1_accumulate", t0, (8 if self._fresh else 12) * self.layout.n_params, stream)
+            TIMER.stop("k1_accumulate", t0, self._k1_bytes_assign if self._fresh else self._k1_bytes_acc, stream)
         self._fresh = False
         self._covered = 0
         self._pending_zero = False
@@ -289,14 +311,16 @@ class GradientAccumulator:
         ptrs = self._ptr_table
         keep = []
         strides = self.layout.strides
+        dts = self._dtype_table
         for j, p in enumerate(self._plist):
             g = p.grad
             if g is None:
                 raise AccumulatorOverflowError("gradient keys do not match accumulator parameters "
                                                "(a parameter received no gradient)")
-            if g.dtype is not torch.float32 or (g.stride() != strides[j] and not self._same_memory_order(g, j)):
+            if g.dtype is not p.dtype or (g.stride() != strides[j] and not self._same_memory_order(g, j)):
                 g = self._conform(g, j)
                 keep.append(g)
+                dts[j] = N.BF16 if g.dtype == torch.bfloat16 else N.F32
             ptrs[j] = g.data_ptr()
         lp = None
         if loss is not None:
@@ -308,10 +332,11 @@ class GradientAccumulator:
         lf = float(factor if loss_factor is None else loss_factor)
         n = len(self._plist)
         t0 = TIMER.start(stream)
-        N.check(N.lib().mbs_accum_add(self._h, ptrs, 0, n, float(factor), lp, lf, float(loss_weight),
-                                      int(bool(last)), _stream_ptr(stream)), "mbs_accum_add")
+        N.check(self._add(ptrs, dts, 0, n, factor, lp, lf, loss_weight, last, stream), "mbs_accum_add")
+        for j, p in enumerate(self._plist):        # restore the per-parameter dtype codes
+            dts[j] = N.BF16 if p.dtype == torch.bfloat16 else N.F32
         if t0 is not None:
-            TIMER.stop("k1_accumulate", t0, (8 if self._fresh else 12) * self.layout.n_params, stream)
+            TIMER.stop("k1_accumulate", t0, self._k1_bytes_assign if self._fresh else self._k1_bytes_acc, stream)
         self._fresh = False
         self._covered = 0
         self._pending_zero = False
@@ -335,7 +360,7 @@ class GradientAccumulator:
                 if g is None:
                     raise AccumulatorOverflowError("gradient keys do not match accumulator parameters "
                                                    "(a parameter received no gradient)")
-                g = self._conform(g, j)
+                g = self._conform(g, j, allow_bf16=False)
                 keep.append(g)
                 ptrs[j] = g.data_ptr()
         lp = None

@@ -91,6 +91,12 @@ def _stream_ptr(stream=None) -> int:
     return (stream or torch.cuda.current_stream()).cuda_stream
 
 
+def _shadow_ptr(params: ParameterSet):
+    """The bf16 shadow K3 refreshes in the same pass (shadow-weight mode), else None."""
+    sh = getattr(params, "shadow", None)
+    return sh.data_ptr() if sh is not None else None
+
+
 def _guard_ptr(grads: GradientSet):
     return grads.norm2.data_ptr() if grads.norm2 is not None else None
 
@@ -103,7 +109,7 @@ def sgd_step(params: ParameterSet, grads: GradientSet, state: OptimizerState, *,
     t0 = TIMER.start(stream)
     N.check(N.lib().mbs_sgd_step(params.flat.data_ptr(), g.data_ptr(), v.data_ptr(), params.layout.total,
                                  float(state.lr), float(state.momentum), float(state.weight_decay),
-                                 _guard_ptr(grads), _stream_ptr(stream)), "mbs_sgd_step")
+                                 _guard_ptr(grads), _shadow_ptr(params), _stream_ptr(stream)), "mbs_sgd_step")
     TIMER.stop("k3_sgd", t0, 20 * params.layout.n_params, stream)
     state.step_count += 1
 
@@ -118,7 +124,7 @@ def adam_step(params: ParameterSet, grads: GradientSet, state: OptimizerState, *
     N.check(N.lib().mbs_adam_step(params.flat.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(),
                                   params.layout.total, float(state.lr), float(state.adam_beta1),
                                   float(state.adam_beta2), float(state.adam_eps), float(state.weight_decay), t,
-                                  _guard_ptr(grads), _stream_ptr(stream)), "mbs_adam_step")
+                                  _guard_ptr(grads), _shadow_ptr(params), _stream_ptr(stream)), "mbs_adam_step")
     TIMER.stop("k3_adam", t0, 28 * params.layout.n_params, stream)
     state.step_count = t
 

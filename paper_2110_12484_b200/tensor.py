@@ -78,8 +78,17 @@ class ParameterSet:
     """
 
     def __init__(self, module: torch.nn.Module | None = None, *, layout: ParamLayout | None = None,
-                 flat: torch.Tensor | None = None, device=None):
+                 flat: torch.Tensor | None = None, device=None, shadow: torch.dtype | None = None):
+        """``shadow=torch.bfloat16``: bf16 shadow-weight mode for bf16-autocast training. Every matmul
+        weight (``dim >= 2``: conv / linear) of the module is replaced by a bf16 Parameter viewing a
+        flat bf16 shadow of the fp32 master buffer; the forward reads it directly (no per-forward
+        autocast cast), its gradient stays bf16 (no fp32 conversion pass: K1 widens it), and the
+        optimizer step (K3) writes the rounded bf16 copy of the updated master in the same pass.
+        ``params[name]`` keeps returning the fp32 master. Call ``sync_shadow()`` after modifying
+        masters outside the optimizer (``load_`` does it)."""
         self.module = module
+        self.shadow = None
+        self.grad_params = None
         if module is not None:
             named = [(n, p) for n, p in module.named_parameters() if p.requires_grad]
             if not named:
@@ -100,6 +109,20 @@ class ParameterSet:
                     v.copy_(p.data)
                     p.data = v
                     self._params[n] = p
+            self.grad_params = [p for _, p in named]
+            if shadow is not None:
+                if shadow != torch.bfloat16:
+                    raise ValueError("shadow weights are bfloat16")
+                self.shadow = torch.zeros(self.layout.total, dtype=torch.bfloat16, device=dev)
+                for i, (n, p) in enumerate(named):
+                    if p.dim() < 2:
+                        continue
+                    owner, _, attr = n.rpartition(".")
+                    sub = module.get_submodule(owner) if owner else module
+                    sp = torch.nn.Parameter(self.layout.view(self.shadow, i))
+                    setattr(sub, attr, sp)
+                    self.grad_params[i] = sp
+                self.sync_shadow()
         else:
             if layout is None or flat is None:
                 raise ValueError("ParameterSet needs a module, or a layout and a flat buffer")
@@ -136,16 +159,24 @@ class ParameterSet:
     def __iter__(self):
         return iter(self.layout.names)
 
+    def sync_shadow(self) -> None:
+        """Refresh the bf16 shadow from the fp32 masters (round-to-nearest-even, like autocast's cast)."""
+        if self.shadow is not None:
+            with torch.no_grad():
+                self.shadow.copy_(self.flat)
+
     def load_(self, other: "ParameterSet | dict") -> None:
         """Copy values in (from a snapshot or a name -> tensor/array dict)."""
         with torch.no_grad():
             if isinstance(other, ParameterSet) and other.layout == self.layout:
                 self.flat.copy_(other.flat)
+                self.sync_shadow()
                 return
             for i, n in enumerate(self.layout.names):
                 src = other[n]
                 src = src.data if isinstance(src, torch.nn.Parameter) else src
                 self.layout.view(self.flat, i).copy_(torch.as_tensor(src))
+        self.sync_shadow()
 
     @property
     def device(self):

@@ -23,7 +23,7 @@ w = WORKLOADS[args.config]
 dev = torch.device("cuda:0")
 torch.backends.cudnn.benchmark = True
 model = build_model(w, ops=args.model_ops).to(dev).to(memory_format=torch.channels_last)
-params = mbs.ParameterSet(model)
+params = mbs.ParameterSet(model, shadow=torch.bfloat16)
 plan = mbs.plan_split(w.mini, w.micro)
 x, y = synthetic_data(w, w.mini, device="cpu" if args.host else dev)
 if args.host:
