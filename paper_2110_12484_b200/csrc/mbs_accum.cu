@@ -45,6 +45,18 @@ constexpr int kMaxPtrs = 1024;     // gradient pointers per K1 launch (kernel-pa
 #define MBS_K1_MINBLOCKS 4
 #endif
 constexpr int kUnroll = MBS_K1_UNROLL;
+// bf16-gradient (shadow-weight) path, A/B in the C2 pipeline (profiles/r01_k1_bf16_ab.txt): 8-byte
+// bf16x4 loads with the 64-register cap (38.8 us/launch, 0.89 of the copy peak) beat 16-byte bf16x8
+// loads at 3 CTAs/SM (46.2 us) or 2 CTAs/SM (42.9 us).
+#ifndef MBS_K1_MIXED_MINBLOCKS
+#define MBS_K1_MIXED_MINBLOCKS 4
+#endif
+#ifndef MBS_K1_U8
+#define MBS_K1_U8 2
+#endif
+#ifndef MBS_K1_BF16_X4
+#define MBS_K1_BF16_X4 1
+#endif
 
 struct Seg {
     int64_t off;   // element offset of the segment in acc (multiple of 4)
@@ -124,44 +136,99 @@ __device__ __forceinline__ int find_seg(const Seg* __restrict__ segs, int s0, in
 
 // One contiguous piece of one segment: acc[0..n) (+)= s * g[0..n). Pieces never exceed one CTA
 // share (<= 2^31 elements), so the inner loops use 32-bit indices (keeps K1 at ~56 registers).
+__device__ __forceinline__ void ld_stream_bf16x8(const uint4* p, float4& lo, float4& hi) {
+    uint32_t a, b, c, d;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p));
+    lo = make_float4(__uint_as_float(a << 16), __uint_as_float(a & 0xffff0000u), __uint_as_float(b << 16),
+                     __uint_as_float(b & 0xffff0000u));
+    hi = make_float4(__uint_as_float(c << 16), __uint_as_float(c & 0xffff0000u), __uint_as_float(d << 16),
+                     __uint_as_float(d & 0xffff0000u));
+}
+
+template <bool ASSIGN>
+__device__ __forceinline__ float4 axpy4(float s, float4 g, float4 a) {
+    float4 r;
+    if (ASSIGN) {
+        r.x = s * g.x; r.y = s * g.y; r.z = s * g.z; r.w = s * g.w;
+    } else {
+        r.x = fmaf(s, g.x, a.x); r.y = fmaf(s, g.y, a.y); r.z = fmaf(s, g.z, a.z); r.w = fmaf(s, g.w, a.w);
+    }
+    return r;
+}
+
 template <bool ASSIGN, bool NORM, typename G>
 __device__ __forceinline__ void accum_piece(float* __restrict__ a, const G* __restrict__ g, int n, float s,
                                             double& sq) {
-    constexpr int kAlign = sizeof(G) == 4 ? 15 : 7;   // 16-byte float4 / 8-byte bf16x4 loads
     int done = 0;
-    if ((reinterpret_cast<uintptr_t>(g) & kAlign) == 0) {
-        const int n4 = n >> 2;
-        float4* a4 = reinterpret_cast<float4*>(a);
-        for (int base = threadIdx.x; base < n4; base += kThreads * kUnroll) {
-            float4 gv[kUnroll], av[kUnroll];
+    float4* a4 = reinterpret_cast<float4*>(a);
+    if constexpr (sizeof(G) == 4) {
+        if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+            const int n4 = n >> 2;
+            for (int base = threadIdx.x; base < n4; base += kThreads * kUnroll) {
+                float4 gv[kUnroll], av[kUnroll];
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
-                const int i = base + u * kThreads;
-                if (i < n4) {
-                    if constexpr (sizeof(G) == 4)
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int i = base + u * kThreads;
+                    if (i < n4) {
                         gv[u] = ld_stream(reinterpret_cast<const float4*>(g) + i);
-                    else
-                        gv[u] = ld_stream_bf16x4(reinterpret_cast<const uint2*>(g) + i);
-                    if (!ASSIGN) av[u] = ld_acc(a4 + i);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
-                const int i = base + u * kThreads;
-                if (i < n4) {
-                    float4 r;
-                    if (ASSIGN) {
-                        r.x = s * gv[u].x; r.y = s * gv[u].y; r.z = s * gv[u].z; r.w = s * gv[u].w;
-                    } else {
-                        r.x = fmaf(s, gv[u].x, av[u].x); r.y = fmaf(s, gv[u].y, av[u].y);
-                        r.z = fmaf(s, gv[u].z, av[u].z); r.w = fmaf(s, gv[u].w, av[u].w);
+                        if (!ASSIGN) av[u] = ld_acc(a4 + i);
                     }
-                    a4[i] = r;
-                    if (NORM) sq += sq4(r);
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int i = base + u * kThreads;
+                    if (i < n4) {
+                        const float4 r = axpy4<ASSIGN>(s, gv[u], av[u]);
+                        a4[i] = r;
+                        if (NORM) sq += sq4(r);
+                    }
                 }
             }
+            done = n4 << 2;
         }
-        done = n4 << 2;
+    } else {
+        // bf16: 8 gradients per 16-byte load against two float4 of the accumulator, so a thread keeps as
+        // many bytes in flight as the fp32 path
+        constexpr int kU8 = MBS_K1_U8;   // only instantiated in the MIXED kernel
+        if (!MBS_K1_BF16_X4 && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+            const int n8 = n >> 3;
+            for (int base = threadIdx.x; base < n8; base += kThreads * kU8) {
+                float4 gl[kU8], gh[kU8], al[kU8], ah[kU8];
+#pragma unroll
+                for (int u = 0; u < kU8; ++u) {
+                    const int i = base + u * kThreads;
+                    if (i < n8) {
+                        ld_stream_bf16x8(reinterpret_cast<const uint4*>(g) + i, gl[u], gh[u]);
+                        if (!ASSIGN) {
+                            al[u] = ld_acc(a4 + 2 * i);
+                            ah[u] = ld_acc(a4 + 2 * i + 1);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kU8; ++u) {
+                    const int i = base + u * kThreads;
+                    if (i < n8) {
+                        const float4 rl = axpy4<ASSIGN>(s, gl[u], al[u]);
+                        const float4 rh = axpy4<ASSIGN>(s, gh[u], ah[u]);
+                        a4[2 * i] = rl;
+                        a4[2 * i + 1] = rh;
+                        if (NORM) sq += sq4(rl) + sq4(rh);
+                    }
+                }
+            }
+            done = n8 << 3;
+        } else if ((reinterpret_cast<uintptr_t>(g) & 7) == 0) {
+            const int n4 = n >> 2;
+            for (int i = threadIdx.x; i < n4; i += kThreads) {
+                const float4 gv = ld_stream_bf16x4(reinterpret_cast<const uint2*>(g) + i);
+                const float4 r = axpy4<ASSIGN>(s, gv, ASSIGN ? gv : ld_acc(a4 + i));
+                a4[i] = r;
+                if (NORM) sq += sq4(r);
+            }
+            done = n4 << 2;
+        }
     }
     for (int i = done + threadIdx.x; i < n; i += kThreads) {  // tail / unaligned gradient
         float gi;
@@ -171,8 +238,10 @@ __device__ __forceinline__ void accum_piece(float* __restrict__ a, const G* __re
         if (NORM) sq += (double)r * (double)r;
     }
 }
-template <bool ASSIGN, bool NORM>
-__global__ void __launch_bounds__(kThreads, MBS_K1_MINBLOCKS)
+// MIXED: the launch has bf16 segments (shadow-weight mode); compiled with a larger register budget
+// (3 CTAs/SM) so the 8-wide bf16 path keeps a full unroll of 16-byte loads in flight without spills.
+template <bool ASSIGN, bool NORM, bool MIXED>
+__global__ void __launch_bounds__(kThreads, MIXED ? MBS_K1_MIXED_MINBLOCKS : MBS_K1_MINBLOCKS)
 k_accum(float* __restrict__ acc, const Seg* __restrict__ segs, const int* __restrict__ tile_seg, int seg0, int seg1,
         int64_t lo0, int64_t hi0, int64_t per_block, const __grid_constant__ GradPtrs gp, float s,
         double* __restrict__ partials,
@@ -193,7 +262,7 @@ k_accum(float* __restrict__ acc, const Seg* __restrict__ segs, const int* __rest
             if (p1 <= p0) continue;
             // bit 0 of a gradient pointer tags bf16 data (bf16 is 2-byte aligned, fp32 4-byte)
             const uintptr_t raw = reinterpret_cast<uintptr_t>(gp.p[si - seg0]);
-            if (raw & 1)
+            if (MIXED && (raw & 1))
                 accum_piece<ASSIGN, NORM>(acc + p0, reinterpret_cast<const __nv_bfloat16*>(raw & ~(uintptr_t)1) +
                                                         (p0 - sg.off), (int)(p1 - p0), s, sq);
             else
@@ -503,7 +572,7 @@ int mbs_accum_create(float* acc_dev, int64_t acc_numel, int64_t n_segments,
     // one full-range launch = exactly the resident CTAs of the device: every CTA gets the same
     // share of elements, so there is no tail wave
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accum<false, true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accum<false, true, false>, kThreads, 0);
     h->grid = std::max(1, per_sm) * sm_count();
     if (const char* t = getenv("MBS_K1_TILE")) h->tile = atoll(t);
     if (h->tile > 0 && h->tile < 1024) h->tile = 1024;
@@ -591,8 +660,10 @@ static int launch_accum(mbs_accum_t h, const void* const* grads, const int* dtyp
     for (int64_t b = 0; b < seg_count; b += kMaxPtrs) {
         const int64_t cnt = std::min<int64_t>(kMaxPtrs, seg_count - b);
         GradPtrs gp;
+        bool mixed = false;
         for (int64_t i = 0; i < cnt; ++i) {
             const bool bf = dtypes != nullptr && dtypes[b + i] == MBS_BF16;
+            mixed |= bf;
             gp.p[i] = reinterpret_cast<const float*>(reinterpret_cast<uintptr_t>(grads[b + i]) | (bf ? 1u : 0u));
         }
         const int s0 = (int)(seg_begin + b), s1 = (int)(seg_begin + b + cnt);
@@ -605,14 +676,21 @@ static int launch_accum(mbs_accum_t h, const void* const* grads, const int* dtyp
         double* ls = h->d_losses + slot;
         double* fs = h->d_factors + slot;
         double* ws = h->d_weights + slot;
-        if (assign && norm)
-            k_accum<true, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, ts, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
-        else if (assign)
-            k_accum<true, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, ts, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
-        else if (norm)
-            k_accum<false, true><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, ts, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
-        else
-            k_accum<false, false><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, ts, s0, s1, lo, hi, per, gp, s, h->d_partials, lp, ls, fs, factor, ws, weight);
+#define MBS_K1_LAUNCH(A, NM, MX)                                                                          \
+    k_accum<A, NM, MX><<<grid, kThreads, 0, st>>>(h->acc, h->d_segs, ts, s0, s1, lo, hi, per, gp, s, h->d_partials, \
+                                                  lp, ls, fs, factor, ws, weight)
+        if (mixed) {
+            if (assign && norm) MBS_K1_LAUNCH(true, true, true);
+            else if (assign) MBS_K1_LAUNCH(true, false, true);
+            else if (norm) MBS_K1_LAUNCH(false, true, true);
+            else MBS_K1_LAUNCH(false, false, true);
+        } else {
+            if (assign && norm) MBS_K1_LAUNCH(true, true, false);
+            else if (assign) MBS_K1_LAUNCH(true, false, false);
+            else if (norm) MBS_K1_LAUNCH(false, true, false);
+            else MBS_K1_LAUNCH(false, false, false);
+        }
+#undef MBS_K1_LAUNCH
         MBS_CK_LAUNCH("k_accum");
         h->n_partials = norm ? (int)grid : 0;
     }
