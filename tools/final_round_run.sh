@@ -4,12 +4,11 @@ timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py > gpurun_out/final_c2.json 2> gpurun_out/final_c2.err
 timeout 600 python bench.py --config c3 --no-cpu-baseline > gpurun_out/final_c3.json 2> gpurun_out/final_c3.err
 timeout 900 python bench.py --config c5 --no-cpu-baseline > gpurun_out/final_c5.json 2> gpurun_out/final_c5.err
+timeout 1500 python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/final_c4.json 2> gpurun_out/final_c4.err
 timeout 400 python bench.py --impl reference > gpurun_out/final_ref.json 2> gpurun_out/final_ref.err
-timeout 400 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r01_c2_v4_launches.csv python tools/profile_step.py > /dev/null 2>&1
-timeout 500 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"k_accum|k_stage|k_sgd|k_finalize|k_gather" -o gpurun_out/r01_c2_v4_full python tools/profile_step.py > /dev/null 2>&1
 python -c "
 import json
-for f in ['gpurun_out/final_c2.json','gpurun_out/final_c3.json','gpurun_out/final_c5.json','gpurun_out/final_ref.json']:
+for f in ['gpurun_out/final_c2.json','gpurun_out/final_c3.json','gpurun_out/final_c5.json','gpurun_out/final_c4.json','gpurun_out/final_ref.json']:
     try:
         d=json.load(open(f)); print(f, d['value'], d.get('e2e',{}).get('value'), (d.get('no_stream') or {}).get('value'), (d.get('no_stream_torch_ops') or {}).get('value'), (d.get('roofline') or {}).get('frac'), d.get('clocks'))
     except Exception as e: print(f, 'ERR', e)
