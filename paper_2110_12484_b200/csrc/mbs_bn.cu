@@ -682,12 +682,13 @@ __global__ void __launch_bounds__(kBnThreads, 2) k_bn_tma(
 
 constexpr int kMaxReduceCtas = 2048;  // bounds the partials (workspace) per BatchNorm call
 
-static BnGeom bn_geom(int64_t rows, int64_t C, int V, int64_t min_rows_per_thread, int target_ctas) {
+static BnGeom bn_geom(int64_t rows, int64_t C, int V, int64_t min_rows_per_thread, int target_ctas,
+                      int max_gv = kBnThreads) {
     BnGeom g;
     g.rows = rows;
     g.C = C;
     const int64_t cv = C / V;
-    g.gv = (int)std::min<int64_t>(cv, kBnThreads);
+    g.gv = (int)std::min<int64_t>(cv, max_gv);
     g.rp = kBnThreads / g.gv;
     const int64_t groups = (cv + g.gv - 1) / g.gv;
     const int64_t per_group = std::max<int64_t>(1, target_ctas / groups);
@@ -705,6 +706,11 @@ static int bn_vec(int dtype, int64_t C, const void* const* ptrs, int n) {
     for (int i = 0; i < n; ++i)
         if (ptrs[i] && (reinterpret_cast<uintptr_t>(ptrs[i]) & 15)) return 1;
     return V;
+}
+
+static int stats_max_gv() {  // A/B: MBS_K5_STATS_GV
+    const char* e = getenv("MBS_K5_STATS_GV");
+    return e ? std::max(1, atoi(e)) : 64;
 }
 
 static int64_t bn_groups(const BnGeom& g, int V) { return (g.C / V + g.gv - 1) / g.gv; }
@@ -763,7 +769,11 @@ template <typename T, int V, int MODE, bool RELU, bool RES>
 static cudaError_t launch_reduce(const T* X, const T* DY, const T* R, const float* w, const float* b,
                                  const float* mean, const float* invstd, float2* part, BnGeom& g, cudaStream_t s) {
     auto k = k_bn_reduce<T, V, MODE, RELU, RES>;
-    g = bn_geom(g.rows, g.C, V, MODE == 0 ? 16 : 32, std::min(wave_ctas(k), kMaxReduceCtas));
+    // statistics: at most 64 channel vectors per CTA, so wide layers (C = 1024 / 2048 on few rows) are
+    // split into channel groups instead of into hundreds of row chunks — their per-CTA partials
+    // (8 B per channel) were ~25 % of the input bytes
+    g = bn_geom(g.rows, g.C, V, MODE == 0 ? 16 : 32, std::min(wave_ctas(k), kMaxReduceCtas),
+                MODE == 0 ? stats_max_gv() : kBnThreads);
     return launch_pdl(k, dim3(g.P, (unsigned)bn_groups(g, V)), s, X, DY, R, w, b, mean, invstd, part, g);
 }
 
