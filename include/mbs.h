@@ -279,9 +279,11 @@ int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype
                          void* stream);
 /* Channel-slice copy between channels-last tensors seen as [M, C_total] rows:
  * dst[m, dst_c0 + c] = src[m, src_c0 + c] (+ bias[c], fp32, nullable) for c < C (the U-Net skip join
- * and its backward). */
+ * and its backward). colsum (nullable): fp32 [colsum_rows][C] per-CTA column sums of the copied
+ * values (the ConvTranspose bias gradient; sum the rows), grid = colsum_rows CTAs. */
 int mbs_copy_channels(const void* src, int64_t src_C, int64_t src_c0, void* dst, int64_t dst_C, int64_t dst_c0,
-                      int64_t M, int64_t C, const float* bias, int dtype, void* stream);
+                      int64_t M, int64_t C, const float* bias, float* colsum, int64_t colsum_rows, int dtype,
+                      void* stream);
 
 /* ---------------------------------------------------------------------------
  * Stem im2col (K7) — the model's first (3-channel) convolution as one library

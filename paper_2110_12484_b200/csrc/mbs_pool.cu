@@ -240,10 +240,18 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
 template <typename T, int V, typename I>
 __global__ void __launch_bounds__(kPoolThreads) k_copy_channels(const T* __restrict__ src, I sC, I sc0,
                                                                 T* __restrict__ dst, I dC, I dc0,
-                                                                I M, I C, const float* __restrict__ bias) {
+                                                                I M, I C, const float* __restrict__ bias,
+                                                                float* __restrict__ colsum) {
+    // colsum (nullable): per-CTA fp32 column sums of the copied values, [gridDim.x][C] — the ConvTranspose
+    // bias gradient of the U-Net join backward, summed in fixed order without another pass. Needs the
+    // grid-stride step to be a multiple of C / V, so a thread keeps one channel vector (host-checked).
+    __shared__ float red[kPoolThreads * (V > 4 ? 8 : V)];
     cudaGridDependencySynchronize();
     const I cv = C / V;
     const I total = M * cv;
+    float cs[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) cs[i] = 0.f;
     for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
         const I c0 = (t % cv) * V;
         const I m = t / cv;
@@ -254,6 +262,23 @@ __global__ void __launch_bounds__(kPoolThreads) k_copy_channels(const T* __restr
             for (int i = 0; i < V; ++i) v[i] += bias[c0 + i];
         }
         PoolIO<T, V>::store(dst + m * dC + dc0 + c0, v);
+        if (colsum) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) cs[i] += v[i];
+        }
+    }
+    if (colsum) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) red[i * kPoolThreads + threadIdx.x] = cs[i];
+        __syncthreads();
+        // threads t, t + cv, t + 2 cv, ... of this CTA hold the same channel vector
+        if ((I)threadIdx.x < cv) {
+            for (int i = 0; i < V; ++i) {
+                float a = 0.f;
+                for (int j = threadIdx.x; j < kPoolThreads; j += (int)cv) a += red[i * kPoolThreads + j];
+                colsum[(size_t)blockIdx.x * C + threadIdx.x * V + i] = a;
+            }
+        }
     }
 }
 
@@ -359,7 +384,7 @@ static int maxpool_bwd(const void* dy, const uint8_t* idx, void* dx, int dtype, 
 
 template <typename I>
 static int copy_channels(const void* src, int64_t sC, int64_t sc0, void* dst, int64_t dC, int64_t dc0, int64_t M,
-                         int64_t C, const float* bias, int dtype, cudaStream_t cs) {
+                         int64_t C, const float* bias, float* colsum, int dtype, cudaStream_t cs) {
     const int es = dtype == MBS_BF16 ? 2 : 4;
     const int V = 16 / es;
     const bool vec = C % V == 0 && sC % V == 0 && dC % V == 0 && sc0 % V == 0 && dc0 % V == 0 &&
@@ -368,14 +393,14 @@ static int copy_channels(const void* src, int64_t sC, int64_t sc0, void* dst, in
     if (dtype == MBS_BF16) {
         using T = __nv_bfloat16;
         e = vec ? pool_launch(k_copy_channels<T, 8, I>, M * (C / 8), cs, (const T*)src, (I)sC, (I)sc0, (T*)dst, (I)dC,
-                              (I)dc0, (I)M, (I)C, bias)
+                              (I)dc0, (I)M, (I)C, bias, colsum)
                 : pool_launch(k_copy_channels<T, 1, I>, M * C, cs, (const T*)src, (I)sC, (I)sc0, (T*)dst, (I)dC, (I)dc0,
-                              (I)M, (I)C, bias);
+                              (I)M, (I)C, bias, colsum);
     } else {
         e = vec ? pool_launch(k_copy_channels<float, 4, I>, M * (C / 4), cs, (const float*)src, (I)sC, (I)sc0,
-                              (float*)dst, (I)dC, (I)dc0, (I)M, (I)C, bias)
+                              (float*)dst, (I)dC, (I)dc0, (I)M, (I)C, bias, colsum)
                 : pool_launch(k_copy_channels<float, 1, I>, M * C, cs, (const float*)src, (I)sC, (I)sc0, (float*)dst,
-                              (I)dC, (I)dc0, (I)M, (I)C, bias);
+                              (I)dC, (I)dc0, (I)M, (I)C, bias, colsum);
     }
     MBS_CK(e);
     return MBS_OK;
@@ -423,7 +448,8 @@ int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype
 }
 
 int mbs_copy_channels(const void* src, int64_t src_C, int64_t src_c0, void* dst, int64_t dst_C, int64_t dst_c0,
-                      int64_t M, int64_t C, const float* bias, int dtype, void* stream) {
+                      int64_t M, int64_t C, const float* bias, float* colsum, int64_t colsum_rows, int dtype,
+                      void* stream) {
     if (!src || !dst) return invalid("mbs_copy_channels: null pointer");
     if (dtype != MBS_BF16 && dtype != MBS_F32) return invalid("mbs_copy_channels: dtype must be MBS_BF16 or MBS_F32");
     if (M < 0 || C < 1 || src_c0 < 0 || dst_c0 < 0 || src_c0 + C > src_C || dst_c0 + C > dst_C)
@@ -431,8 +457,39 @@ int mbs_copy_channels(const void* src, int64_t src_C, int64_t src_c0, void* dst,
     if (M == 0) return MBS_OK;
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     const bool i32 = fits_i32(M * std::max(src_C, dst_C));
-    return i32 ? copy_channels<int32_t>(src, src_C, src_c0, dst, dst_C, dst_c0, M, C, bias, dtype, cs)
-               : copy_channels<int64_t>(src, src_C, src_c0, dst, dst_C, dst_c0, M, C, bias, dtype, cs);
+    if (colsum) {
+        // one thread per channel vector for the whole grid-stride: C/V must divide the CTA size, the grid is
+        // exactly colsum_rows CTAs (the caller sums the [colsum_rows][C] partials)
+        const int V = dtype == MBS_BF16 ? 8 : 4;
+        const int64_t cv = C / V;
+        if (C % V || kPoolThreads % cv || colsum_rows < 1)
+            return invalid("mbs_copy_channels: colsum needs C/V to divide 256 and colsum_rows >= 1");
+        if (!aligned16(src, dst, nullptr) || src_C % V || dst_C % V || src_c0 % V || dst_c0 % V)
+            return invalid("mbs_copy_channels: colsum needs the vector path (16-byte aligned columns)");
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)colsum_rows);
+        cfg.blockDim = dim3(kPoolThreads);
+        cfg.stream = cs;
+        cudaError_t e;
+        if (dtype == MBS_BF16) {
+            using T = __nv_bfloat16;
+            e = i32 ? cudaLaunchKernelEx(&cfg, k_copy_channels<T, 8, int32_t>, (const T*)src, (int32_t)src_C,
+                                         (int32_t)src_c0, (T*)dst, (int32_t)dst_C, (int32_t)dst_c0, (int32_t)M,
+                                         (int32_t)C, bias, colsum)
+                    : cudaLaunchKernelEx(&cfg, k_copy_channels<T, 8, int64_t>, (const T*)src, src_C, src_c0, (T*)dst,
+                                         dst_C, dst_c0, M, C, bias, colsum);
+        } else {
+            e = i32 ? cudaLaunchKernelEx(&cfg, k_copy_channels<float, 4, int32_t>, (const float*)src, (int32_t)src_C,
+                                         (int32_t)src_c0, (float*)dst, (int32_t)dst_C, (int32_t)dst_c0, (int32_t)M,
+                                         (int32_t)C, bias, colsum)
+                    : cudaLaunchKernelEx(&cfg, k_copy_channels<float, 4, int64_t>, (const float*)src, src_C, src_c0,
+                                         (float*)dst, dst_C, dst_c0, M, C, bias, colsum);
+        }
+        MBS_CK(e);
+        return MBS_OK;
+    }
+    return i32 ? copy_channels<int32_t>(src, src_C, src_c0, dst, dst_C, dst_c0, M, C, bias, nullptr, dtype, cs)
+               : copy_channels<int64_t>(src, src_C, src_c0, dst, dst_C, dst_c0, M, C, bias, nullptr, dtype, cs);
 }
 
 }  // extern "C"

@@ -109,11 +109,16 @@ class _PoolStashFn(torch.autograd.Function):
         return dx, None, None
 
 
-def _copy_channels(src, s_c, s_c0, dst, d_c, d_c0, m, c, bias):
+_COLSUM_CTAS = 2 * 148
+
+
+def _copy_channels(src, s_c, s_c0, dst, d_c, d_c0, m, c, bias, colsum=None):
     stream = torch.cuda.current_stream(src.device)
     TIMER.launches += 1
     _native.check(_native.lib().mbs_copy_channels(src.data_ptr(), s_c, s_c0, dst.data_ptr(), d_c, d_c0, m, c,
-                                                  None if bias is None else bias.data_ptr(), _DTYPES[src.dtype],
+                                                  None if bias is None else bias.data_ptr(),
+                                                  None if colsum is None else colsum.data_ptr(),
+                                                  0 if colsum is None else colsum.shape[0], _DTYPES[src.dtype],
                                                   stream.cuda_stream), "mbs_copy_channels")
 
 
@@ -141,9 +146,14 @@ class _JoinFn(torch.autograd.Function):
         g = g.contiguous(memory_format=torch.channels_last)
         cu = ctot - cs
         gup = torch.empty((n, cu, h, w), dtype=g.dtype, device=g.device, memory_format=torch.channels_last)
-        _copy_channels(g, ctot, cs, gup, cu, 0, n * h * w, cu, None)
-        # fp32 accumulation without materialising an fp32 copy of the slice
-        gb = gup.sum(dim=(0, 2, 3), dtype=torch.float32) if has_bias and ctx.needs_input_grad[2] else None
+        v = 16 // g.element_size()
+        fuse = (has_bias and ctx.needs_input_grad[2] and cu % v == 0 and 256 % (cu // v) == 0
+                and ctot % v == 0 and cs % v == 0 and g.data_ptr() % 16 == 0)
+        parts = torch.empty((_COLSUM_CTAS, cu), dtype=torch.float32, device=g.device) if fuse else None
+        _copy_channels(g, ctot, cs, gup, cu, 0, n * h * w, cu, None, parts)
+        gb = None
+        if has_bias and ctx.needs_input_grad[2]:   # the bias gradient: column sums taken during the copy
+            gb = parts.sum(0) if fuse else gup.sum(dim=(0, 2, 3), dtype=torch.float32)
         return g, gup, gb, None
 
 
