@@ -710,7 +710,7 @@ static int bn_vec(int dtype, int64_t C, const void* const* ptrs, int n) {
 
 static int stats_max_gv() {  // A/B: MBS_K5_STATS_GV
     const char* e = getenv("MBS_K5_STATS_GV");
-    return e ? std::max(1, atoi(e)) : 64;
+    return e ? std::max(1, atoi(e)) : 32;
 }
 
 static int64_t bn_groups(const BnGeom& g, int V) { return (g.C / V + g.gv - 1) / g.gv; }
@@ -769,7 +769,7 @@ template <typename T, int V, int MODE, bool RELU, bool RES>
 static cudaError_t launch_reduce(const T* X, const T* DY, const T* R, const float* w, const float* b,
                                  const float* mean, const float* invstd, float2* part, BnGeom& g, cudaStream_t s) {
     auto k = k_bn_reduce<T, V, MODE, RELU, RES>;
-    // statistics: at most 64 channel vectors per CTA, so wide layers (C = 1024 / 2048 on few rows) are
+    // statistics: at most 32 channel vectors per CTA (A/B: profiles/r01_k5_stats_gv_ab.txt), so wide layers (C = 1024 / 2048 on few rows) are
     // split into channel groups instead of into hundreds of row chunks — their per-CTA partials
     // (8 B per channel) were ~25 % of the input bytes
     g = bn_geom(g.rows, g.C, V, MODE == 0 ? 16 : 32, std::min(wave_ctas(k), kMaxReduceCtas),
