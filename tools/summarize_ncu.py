@@ -59,11 +59,11 @@ for r in recs:
               f"{r['dram__bytes_write.sum']:.1f} | {r['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']:.1f} | "
               f"{r['launch__registers_per_thread']:.0f} | {r['sm__warps_active.avg.pct_of_peak_sustained_active']:.1f} |")
 open(f"profiles/{tag}_ncu_full.md", "w").write("\n".join(md) + "\n")
-acc = [r for r in recs if "k_accum<0, 0>" in r["Kernel Name"]]
+acc = [r for r in recs if "k_accum<0, 0" in r["Kernel Name"]]   # acc += s*g (fp32 or MIXED bf16 grads)
 if acc:
     mb = (acc[0]["dram__bytes_read.sum"] + acc[0]["dram__bytes_write.sum"])
     scale = 1e6 if units[idx.index(hh.index("dram__bytes_read.sum"))] == "Mbyte" else 1.0
-    json.dump({"kernel": "k_accum<0,0> (acc += s*g)", "dram_bytes_per_launch": mb * scale,
+    json.dump({"kernel": acc[0]["Kernel Name"][:40] + " (acc += s*g)", "dram_bytes_per_launch": mb * scale,
                "source": f"profiles/{tag}_ncu_full.json"}, open("profiles/ncu_k1_traffic.json", "w"), indent=1)
 print("\n".join(lines[:8]))
 print("\n".join(md))
