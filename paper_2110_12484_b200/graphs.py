@@ -32,6 +32,7 @@ import torch
 from .losses import compute_loss
 
 _CACHE: dict = {}
+MAX_GRAPHS = 8          # captured steps kept (each holds its model and a private memory pool); oldest evicted
 
 
 class MicroStepGraph:
@@ -111,6 +112,9 @@ def graph_for(model, plist, loss_kind, xk, yk, autocast_dtype, loss_from_logits,
            autocast_dtype, bool(loss_from_logits), float(dice_smoothing), tuple(p.data_ptr() for p in plist[:4]))
     g = _CACHE.get(key)
     if g is None:
+        while len(_CACHE) >= MAX_GRAPHS:
+            _CACHE.pop(next(iter(_CACHE)))
+            torch.cuda.empty_cache()
         g = _CACHE[key] = MicroStepGraph(model, plist, loss_kind, xk, yk, autocast_dtype, loss_from_logits,
                                          dice_smoothing)
     return g
