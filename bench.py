@@ -417,10 +417,12 @@ def main():
             "config": {"workload": w.name, "model": w.model, "mini_batch_per_gpu": n_b, "micro_batch": n_mu,
                        "n_micro": plan.n_s_mu, "global_batch": n_b * ws, "parallelism": f"dp{ws}",
                        "normalization": w.normalization, "optimizer": w.optimizer,
-                       "model_precision": "bf16 autocast on cuDNN/cuBLAS, fp32 master weights; MBS path fp32",
-                       "model_ops": ("BatchNorm(+ReLU/+skip add) on K5 and max-pool on K6 sm_100a kernels "
-                                     "(bn.py, pool.py), micro-batch statistics" if args.model_ops == "native"
-                                     else "stock torch BatchNorm / max-pool"),
+                       "model_precision": "bf16 compute (autocast) on cuDNN/cuBLAS reading bf16 shadow weights that "
+                                          "K3 writes; fp32 master weights, fp32 MBS accumulation",
+                       "model_ops": ("BatchNorm(+ReLU/+skip add) on K5, max-pool (+U-Net skip join) on K6, stem "
+                                     "conv as K7 im2col + GEMM (bn.py, pool.py, stem.py), micro-batch statistics; "
+                                     "micro step replayed from a CUDA graph" if args.model_ops == "native"
+                                     else "stock torch BatchNorm / max-pool / stem conv"),
                        "input": "uint8 NCHW staged to bf16 NHWC by K2",
                        "l2": ("inputs > L2: every mini-batch is %.0f MB of uint8" % (x_dev[:n_b].numel() / 1e6)) +
                              ", none reused within the timed region",
