@@ -35,7 +35,7 @@ import numpy as np
 import torch
 
 from .engine import (GradientAccumulator, MicroBatchPlan, MiniBatchStats, _as_tensor, _micro_source, make_streamer,
-                     normalization_factor, plan_split, weight_cast_cache)
+                     normalization_factor, plan_split, weight_cast_cache, _graph_for)
 from .losses import compute_loss
 from .optim import apply_update
 from .tensor import ParameterSet
@@ -391,19 +391,31 @@ class DataParallelMBS:
         cast_cache.__enter__()
         try:
             self._micro_loop(model, plan, block, source, normalization, loss_kind, acc, ctx, loss_from_logits,
-                             dice_smoothing, n_local, losses, factors, weights, works, plist)
+                             dice_smoothing, n_local, losses, factors, weights, works, plist, autocast_dtype)
         finally:
             cast_cache.__exit__(None, None, None)
         return self._exchange_and_step(model, plan, block, optimizer_state, acc, n_local, losses, factors, weights,
                                        works, bn, lr_for_step)
 
     def _micro_loop(self, model, plan, block, source, normalization, loss_kind, acc, ctx, loss_from_logits,
-                    dice_smoothing, n_local, losses, factors, weights, works, plist):
+                    dice_smoothing, n_local, losses, factors, weights, works, plist, autocast_dtype=None):
         for j in range(n_local):
             xk, yk = next(source)
             k = block[0] + j
             f = normalization_factor(plan, k, normalization)
             last = j == n_local - 1
+            if not last:
+                # every micro-batch but the rank's last replays the captured micro step (engine.py); the
+                # last interleaves K1 buckets and all-reduces with its backward through hooks: eager
+                g = _graph_for(model, acc, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing,
+                               "fused", False, headroom=2.3)
+                if g is not None:
+                    loss = g.replay(xk, yk)
+                    losses.append(loss.detach().float().clone())   # the static loss is overwritten next replay
+                    factors.append(f)
+                    weights.append(float(plan.sizes[k]))
+                    acc.add_pointer_table(g.ptrs, f, loss=loss, loss_factor=f, loss_weight=plan.sizes[k])
+                    continue
             with ctx:
                 out = model(xk)
                 loss = compute_loss(loss_kind, out, yk, from_logits=loss_from_logits, dice_smoothing=dice_smoothing)

@@ -610,7 +610,7 @@ _NO_GRAPH: set = set()
 
 
 def _graph_for(model, acc, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing, normalize_via,
-               keep_outputs):
+               keep_outputs, headroom: float = 1.15):
     """The captured micro step for this micro-batch shape, or None to run eagerly.
 
     Graphs need: CUDA inputs, training mode, the factor applied by K1 (normalize_via "fused") and
@@ -623,7 +623,8 @@ def _graph_for(model, acc, loss_kind, xk, yk, autocast_dtype, loss_from_logits, 
         return None
     from . import graphs
     try:
-        g = graphs.graph_for(model, acc._plist, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing)
+        g = graphs.graph_for(model, acc._plist, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing,
+                             headroom=headroom)
     except Exception as e:                 # noqa: BLE001 - capture limits: fall back to eager, loudly
         import warnings
         if not isinstance(e, MemoryError):

@@ -37,7 +37,7 @@ MAX_GRAPHS = 8          # captured steps kept (each holds its model and a privat
 
 class MicroStepGraph:
     def __init__(self, model, plist, loss_kind, x_like, y_like, autocast_dtype, loss_from_logits, dice_smoothing,
-                 warmup: int = 2):
+                 warmup: int = 2, headroom: float = 1.15):
         dev = x_like.device
         fmt = torch.channels_last if (x_like.dim() == 4 and x_like.is_contiguous(memory_format=torch.channels_last)
                                       and not x_like.is_contiguous()) else torch.contiguous_format
@@ -80,7 +80,7 @@ class MicroStepGraph:
         torch.cuda.empty_cache()           # warm-up blocks back to the driver before the private pool grows
         need = torch.cuda.max_memory_allocated(dev) - base
         free = torch.cuda.mem_get_info(dev)[0]
-        if free < 1.15 * need + (1 << 30):
+        if free < headroom * need + (1 << 30):
             # the private pool would not fit next to the eager allocator's blocks (e.g. a micro-batch
             # auto-sized to fill HBM): keep this shape eager
             raise MemoryError(f"graph pool needs ~{need / 2**30:.1f} GiB, {free / 2**30:.1f} GiB free")
@@ -107,7 +107,10 @@ class MicroStepGraph:
         return self.loss
 
 
-def graph_for(model, plist, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing) -> MicroStepGraph:
+def graph_for(model, plist, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing,
+              headroom: float = 1.15) -> MicroStepGraph:
+    """The cached capture for this micro shape; ``headroom`` x the step's activation bytes must be free
+    (2.3 when an eager step of the same size must still fit next to the pool, e.g. the DP last micro)."""
     key = (id(model), tuple(xk.shape), xk.dtype, xk.is_contiguous(), tuple(yk.shape), yk.dtype, loss_kind,
            autocast_dtype, bool(loss_from_logits), float(dice_smoothing), tuple(p.data_ptr() for p in plist[:4]))
     g = _CACHE.get(key)
@@ -116,7 +119,7 @@ def graph_for(model, plist, loss_kind, xk, yk, autocast_dtype, loss_from_logits,
             _CACHE.pop(next(iter(_CACHE)))
             torch.cuda.empty_cache()
         g = _CACHE[key] = MicroStepGraph(model, plist, loss_kind, xk, yk, autocast_dtype, loss_from_logits,
-                                         dice_smoothing)
+                                         dice_smoothing, headroom=headroom)
     return g
 
 
