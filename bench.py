@@ -202,7 +202,8 @@ def main():
         else:
             dist.init_process_group(backend)
     torch.cuda.set_device(dev)
-    torch.backends.cudnn.benchmark = True
+    torch.backends.cudnn.benchmark = os.environ.get("MBS_BENCH_DETERMINISTIC", "0") != "1"
+    torch.backends.cudnn.deterministic = not torch.backends.cudnn.benchmark   # reproducibility checks only
     torch.manual_seed(1234 + rank)
 
     model = build_model(w, ops=args.model_ops).to(dev).to(memory_format=torch.channels_last)
