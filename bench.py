@@ -382,6 +382,8 @@ def main():
                               "(acc = s*g); P = %d" % params.layout.n_params,
                 "how": "CUDA events around every K1 launch of two extra HBM-resident mini-batches (eager), "
                        "outside the timed region",
+                "note": "K1 is the kernel the north star names (accumulate); the dominant kernel of the step by "
+                        "time is the model's K5 BatchNorm, reported in roofline_k5",
                 "other_kernels": {k: {"gbs": v["gbs"], "avg_us": v["avg_ms"] * 1e3, "launches": v["launches"]}
                                   for k, v in kstats.items() if k != "k1_accumulate"}}
     try:
