@@ -410,7 +410,7 @@ def main():
                        "ms_per_mini_batch": kt, "calls": {k: v["launches"] for k, v in k5stats.items()},
                        "per_call": {k: {"gbs": v["gbs"], "avg_us": v["avg_ms"] * 1e3} for k, v in k5stats.items()},
                        "bytes_rule": "per call over E activation elements of s bytes: forward 3*E*s (+E*s "
-                                     "residual), backward 5*E*s (+3*E*s residual); CUDA events around each "
+                                     "residual), backward 5*E*s (+2*E*s residual: the two-pass minimum); CUDA events around each "
                                      "3-kernel call, so small layers include launch gaps"}
 
     line = {"metric": "effective-batch samples/sec", "value": value, "unit": "samples/s", "n_gpus": ws,

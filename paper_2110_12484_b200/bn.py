@@ -134,8 +134,9 @@ class _MicroBatchNormFn(torch.autograd.Function):
         _native.check(_native.lib().mbs_bn_backward(
             _ptr(x), _ptr(residual), _ptr(dy), _ptr(dx), _ptr(dres), ctx.code, rows, C, _ptr(weight), _ptr(bias),
             _ptr(mean), _ptr(invstd), int(ctx.relu), _ptr(dw), _ptr(db), _ptr(ws), st), "mbs_bn_backward")
-        # algorithmic bytes: reduce read x, dy (+ residual); elemt read x, dy (+ residual), write dx (+ dresidual)
-        TIMER.stop("k5_bn_backward", ev, x.numel() * x.element_size() * (5 + 3 * ctx.has_res), stream)
+        # algorithmic bytes (two-pass minimum): reduce read x, dy (+ residual, + write d_residual = g); elemt read
+        # x and dy (or g), write dx
+        TIMER.stop("k5_bn_backward", ev, x.numel() * x.element_size() * (5 + 2 * ctx.has_res), stream)
         return dx, dres, dw, db, None, None, None, None, None
 
 
