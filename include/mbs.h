@@ -253,11 +253,14 @@ int mbs_bn_forward(const void* x, const void* residual, void* y, int dtype, int6
                    double momentum, double eps, int relu, float* save_mean, float* save_invstd,
                    void* workspace, void* stream);
 /* Gradients of mbs_bn_forward: dx, dresidual (iff residual), dweight/dbias (may be NULL).
- * The ReLU mask is recomputed from x (and residual) bit-identically to the forward. */
-int mbs_bn_backward(const void* x, const void* residual, const void* dy, void* dx, void* dresidual, int dtype,
-                    int64_t rows, int64_t C, const float* weight, const float* bias, const float* save_mean,
-                    const float* save_invstd, int relu, float* dweight, float* dbias, void* workspace,
-                    void* stream);
+ * The ReLU mask is recomputed from x (and residual) bit-identically to the forward.
+ * dy2 (nullable): a second gradient of y (the output feeds both the next block's main path and its
+ * skip), summed with dy in fp32 inside the kernel; only with residual + relu, C/8 (bf16) or C/4 (fp32)
+ * vectors <= 256 and every pointer 16-byte aligned — otherwise MBS_ERR_INVALID. */
+int mbs_bn_backward(const void* x, const void* residual, const void* dy, const void* dy2, void* dx,
+                    void* dresidual, int dtype, int64_t rows, int64_t C, const float* weight, const float* bias,
+                    const float* save_mean, const float* save_invstd, int relu, float* dweight, float* dbias,
+                    void* workspace, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Max-pool (K6) — the model's MaxPool2d in every micro-batch forward/backward,

@@ -78,7 +78,8 @@ _SIGS = {
     "mbs_bn_workspace_bytes": (c_int, [c_int64, c_int64, c_int, POINTER(c_int64)]),
     "mbs_bn_forward": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_double, c_double, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
-    "mbs_bn_backward": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p,
+    "mbs_bn_backward": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64,
+                                c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "mbs_maxpool_forward": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64, c_int,
                                     c_int, c_int, c_void_p, c_int64, c_int64, c_void_p]),

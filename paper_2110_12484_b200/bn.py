@@ -67,6 +67,14 @@ def _n_kernels(C: int, tensors, nbytes: int) -> int:
     return 1 if nbytes <= limit else 3
 
 
+def _dual_ok(C: int, tensors, relu_res: bool) -> bool:
+    """Whether mbs_bn_backward takes a second output gradient (mirrors its dy2 contract in include/mbs.h):
+    the fused residual path with 16-byte channel vectors, <= 256 of them, every pointer 16-byte aligned."""
+    v = 16 // tensors[0].element_size()
+    return (relu_res and C % v == 0 and C // v <= 256
+            and all(t is None or t.data_ptr() % 16 == 0 for t in tensors))
+
+
 def _channels_last(t: torch.Tensor) -> torch.Tensor:
     if t.dim() == 4:
         return t.contiguous(memory_format=torch.channels_last)
@@ -86,7 +94,7 @@ class _MicroBatchNormFn(torch.autograd.Function):
     """y = relu?(bn(x) [+ residual]) with micro-batch statistics; one running-stat update."""
 
     @staticmethod
-    def forward(ctx, x, residual, weight, bias, running_mean, running_var, momentum, eps, relu):
+    def forward(ctx, x, residual, weight, bias, running_mean, running_var, momentum, eps, relu, dual=False):
         code = _DTYPES.get(x.dtype)
         if code is None:
             raise ValueError(f"micro-batch BatchNorm supports bfloat16 / float32 activations, got {x.dtype}")
@@ -115,13 +123,24 @@ class _MicroBatchNormFn(torch.autograd.Function):
         ctx.relu = bool(relu)
         ctx.code = code
         ctx.has_res = residual is not None
+        if dual:
+            # two handles on the same activation: the consumers' gradients reach backward separately
+            # and are summed inside K5's reduce instead of by an autograd add pass
+            ctx.set_materialize_grads(False)
+            return y, y.view_as(y)
         return y
 
     @staticmethod
-    def backward(ctx, dy):
+    def backward(ctx, dy, dy2=None):
         x, residual, weight, bias, mean, invstd = ctx.saved_tensors
+        if dy is None:
+            dy, dy2 = dy2, None
         dy = _channels_last(dy.to(x.dtype))
         rows, C = _geometry(x)
+        if dy2 is not None:
+            dy2 = _channels_last(dy2.to(x.dtype))
+            if not _dual_ok(C, (x, residual, dy, dy2), ctx.relu and ctx.has_res):
+                dy, dy2 = dy + dy2, None
         dx = torch.empty_like(x)
         dres = torch.empty_like(x) if ctx.has_res else None
         dw = torch.empty_like(weight) if weight is not None and ctx.needs_input_grad[2] else None
@@ -129,23 +148,26 @@ class _MicroBatchNormFn(torch.autograd.Function):
         ws = _workspace(rows, C, ctx.code, x.device)
         stream = torch.cuda.current_stream(x.device)
         st = stream.cuda_stream
-        ev = TIMER.start_k5(_n_kernels(C, (x, residual, dy, dx, dres),
-                                       x.numel() * x.element_size() * (2 + ctx.has_res)), stream)
+        ev = TIMER.start_k5(3 if dy2 is not None else
+                            _n_kernels(C, (x, residual, dy, dx, dres), x.numel() * x.element_size() * (2 + ctx.has_res)),
+                            stream)
         _native.check(_native.lib().mbs_bn_backward(
-            _ptr(x), _ptr(residual), _ptr(dy), _ptr(dx), _ptr(dres), ctx.code, rows, C, _ptr(weight), _ptr(bias),
-            _ptr(mean), _ptr(invstd), int(ctx.relu), _ptr(dw), _ptr(db), _ptr(ws), st), "mbs_bn_backward")
-        # algorithmic bytes (two-pass minimum): reduce read x, dy (+ residual, + write d_residual = g); elemt read
-        # x and dy (or g), write dx
-        TIMER.stop("k5_bn_backward", ev, x.numel() * x.element_size() * (5 + 2 * ctx.has_res), stream)
-        return dx, dres, dw, db, None, None, None, None, None
+            _ptr(x), _ptr(residual), _ptr(dy), _ptr(dy2), _ptr(dx), _ptr(dres), ctx.code, rows, C, _ptr(weight),
+            _ptr(bias), _ptr(mean), _ptr(invstd), int(ctx.relu), _ptr(dw), _ptr(db), _ptr(ws), st), "mbs_bn_backward")
+        # algorithmic bytes (two-pass minimum): reduce read x, dy (+ dy2) (+ residual, + write d_residual = g);
+        # elemt read x and dy (or g), write dx
+        TIMER.stop("k5_bn_backward", ev,
+                   x.numel() * x.element_size() * (5 + 2 * ctx.has_res + (dy2 is not None)), stream)
+        return dx, dres, dw, db, None, None, None, None, None, None
 
 
 def micro_batch_norm(x, weight, bias, running_mean=None, running_var=None, *, momentum=0.1, eps=1e-5,
-                     relu=False, residual=None):
-    """Functional form: ``relu?(batch_norm(x, training=True) [+ residual])`` on the native kernels."""
+                     relu=False, residual=None, dual=False):
+    """Functional form: ``relu?(batch_norm(x, training=True) [+ residual])`` on the native kernels
+    (``dual``: the output as two autograd handles, see ``MicroBatchNorm2d.forward``)."""
     if residual is not None and not relu:
         raise ValueError("a residual is only fused together with the ReLU")
-    return _MicroBatchNormFn.apply(x, residual, weight, bias, running_mean, running_var, momentum, eps, relu)
+    return _MicroBatchNormFn.apply(x, residual, weight, bias, running_mean, running_var, momentum, eps, relu, dual)
 
 
 class MicroBatchNorm2d(nn.BatchNorm2d):
@@ -165,13 +187,16 @@ class MicroBatchNorm2d(nn.BatchNorm2d):
     def extra_repr(self):
         return super().extra_repr() + f", fuse_relu={self.fuse_relu}"
 
-    def forward(self, x, residual=None):
+    def forward(self, x, residual=None, dual: bool = False):
+        """``dual``: return the output twice (``(y, y)``, two autograd handles) for an activation with two
+        consumers, so their gradients are summed inside the backward kernel."""
         batch_stats = self.training or not self.track_running_stats
         if not batch_stats:                       # inference normalisation with running statistics
             y = F.batch_norm(x, self.running_mean, self.running_var, self.weight, self.bias, False, 0.0, self.eps)
             if residual is not None:
                 y = y + residual
-            return F.relu(y) if self.fuse_relu else y
+            y = F.relu(y) if self.fuse_relu else y
+            return (y, y) if dual else y
         if not x.is_cuda:
             raise RuntimeError("MicroBatchNorm2d: training-mode normalisation runs on the sm_100a kernels "
                                "(libmbs_native.so) and needs a CUDA tensor; there is no CPU fallback")
@@ -186,7 +211,7 @@ class MicroBatchNorm2d(nn.BatchNorm2d):
         return _MicroBatchNormFn.apply(x, residual, self.weight, self.bias,
                                        self.running_mean if track else None,
                                        self.running_var if track else None,
-                                       momentum, self.eps, self.fuse_relu)
+                                       momentum, self.eps, self.fuse_relu, dual)
 
 
 def _as_micro_bn(bn: nn.BatchNorm2d, relu: bool) -> MicroBatchNorm2d:
@@ -195,17 +220,44 @@ def _as_micro_bn(bn: nn.BatchNorm2d, relu: bool) -> MicroBatchNorm2d:
     return bn
 
 
-def _bottleneck_forward(self, x):
-    identity = x if self.downsample is None else self.downsample(x)
-    out = self.bn1(self.conv1(x))
+def _bottleneck_pair(self, xm, xr, dual):
+    """Block on (main, skip) handles of the same input; returns the output (twice when ``dual``)."""
+    identity = xr if self.downsample is None else self.downsample(xr)
+    out = self.bn1(self.conv1(xm))
     out = self.bn2(self.conv2(out))
-    return self.bn3(self.conv3(out), identity)
+    return self.bn3(self.conv3(out), identity, dual=dual)
+
+
+def _basic_pair(self, xm, xr, dual):
+    identity = xr if self.downsample is None else self.downsample(xr)
+    out = self.bn1(self.conv1(xm))
+    return self.bn2(self.conv2(out), identity, dual=dual)
+
+
+def _bottleneck_forward(self, x):
+    return _bottleneck_pair(self, x, x, False)
 
 
 def _basic_forward(self, x):
-    identity = x if self.downsample is None else self.downsample(x)
-    out = self.bn1(self.conv1(x))
-    return self.bn2(self.conv2(out), identity)
+    return _basic_pair(self, x, x, False)
+
+
+def _resnet_forward(self, x):
+    """torchvision ResNet._forward_impl with every block output but the last handed on as two autograd
+    handles (next block's conv1 and its skip / downsample): the gradient sum of the two consumers
+    happens in K5's backward reduce of the producing block (mbs_bn_backward dy2), not in an autograd add."""
+    x = self.maxpool(self.relu(self.bn1(self.conv1(x))))
+    blocks = [b for layer in (self.layer1, self.layer2, self.layer3, self.layer4) for b in layer]
+    xm = xr = x
+    for i, blk in enumerate(blocks):
+        dual = i + 1 < len(blocks) and isinstance(blk, (FusedBottleneck, FusedBasicBlock))
+        if isinstance(blk, (FusedBottleneck, FusedBasicBlock)):
+            out = blk.forward_pair(xm, xr, dual)
+        else:
+            out = blk(xm)
+        xm, xr = out if dual else (out, out)
+    x = torch.flatten(self.avgpool(xm), 1)
+    return self.fc(x)
 
 
 try:
@@ -214,10 +266,16 @@ try:
     class FusedBottleneck(tv_resnet.Bottleneck):
         """torchvision Bottleneck with bn1/bn2 -> relu and bn3 + identity -> relu on K5."""
         forward = _bottleneck_forward
+        forward_pair = _bottleneck_pair
 
     class FusedBasicBlock(tv_resnet.BasicBlock):
         """torchvision BasicBlock with bn1 -> relu and bn2 + identity -> relu on K5."""
         forward = _basic_forward
+        forward_pair = _basic_pair
+
+    class FusedResNet(tv_resnet.ResNet):
+        """torchvision ResNet whose block outputs reach the next block as two handles (dual K5 output)."""
+        _forward_impl = _resnet_forward
 except ImportError:  # pragma: no cover - torchvision is in the image
     tv_resnet = None
 
@@ -237,6 +295,8 @@ def fuse_batchnorm(model: nn.Module) -> nn.Module:
         elif tv_resnet is not None and type(mod) is tv_resnet.ResNet:
             _as_micro_bn(mod.bn1, True)
             mod.relu = nn.Identity()           # the stem's ReLU (blocks own their own relu modules)
+            if os.environ.get("MBS_K5_DUAL", "1") != "0":   # A/B: MBS_K5_DUAL=0 keeps autograd's adds
+                mod.__class__ = FusedResNet
         elif isinstance(mod, nn.Sequential):
             kids = list(mod._modules.items())
             for i, (name, child) in enumerate(kids):

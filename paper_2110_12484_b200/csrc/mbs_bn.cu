@@ -536,22 +536,29 @@ constexpr int kTmaStages = 4;        // ring depth (A/B on B200: deeper rings of
 constexpr int kTmaTileBytes = 8192;  // per input tensor per stage
 constexpr int kMaxTmaCtas = 4 * 148; // bounds the TMA path's partials (workspace)
 
-template <int KIND, bool RES>
+template <int KIND, bool RES, bool DY2 = false>
 __host__ __device__ constexpr int tma_inputs() {
-    return 1 + ((KIND == 1 || KIND == 3) ? 1 : 0) + (RES ? 1 : 0);
+    return 1 + ((KIND == 1 || KIND == 3) ? 1 : 0) + (RES ? 1 : 0) + (DY2 ? 1 : 0);
 }
 
+// four input tensors: 3 stages, so two CTAs (2 x 96 KB) still fit on an SM
+__host__ __device__ constexpr int tma_stages(int nin) { return nin >= 4 ? 3 : kTmaStages; }
 
-template <typename T, int V, int KIND, bool RELU, bool RES>
+
+// DY2 (KIND 1 only): the output gradient arrives as two tensors (the residual block's two consumers,
+// bn.py dual outputs) and is summed in fp32 on the fly — autograd's separate add pass disappears.
+template <typename T, int V, int KIND, bool RELU, bool RES, bool DY2 = false>
 __global__ void __launch_bounds__(kBnThreads, 2) k_bn_tma(
         const T* __restrict__ x, const T* __restrict__ dy, const T* __restrict__ res, T* __restrict__ out,
         T* __restrict__ dres, const float* __restrict__ w, const float* __restrict__ b,
         const float* __restrict__ mean, const float* __restrict__ invstd, const float* __restrict__ coef,
-        float2* __restrict__ part, BnGeom g, int tile_rows) {
-    constexpr int NIN = tma_inputs<KIND, RES>();
+        float2* __restrict__ part, BnGeom g, int tile_rows, const T* __restrict__ dy2) {
+    static_assert(!DY2 || KIND == 1, "a second output gradient is only read by the backward reduce");
+    constexpr int NIN = tma_inputs<KIND, RES, DY2>();
+    constexpr int STG = tma_stages(NIN);
     constexpr bool kFold = sizeof(T) == 2;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t full[kTmaStages];
+    __shared__ __align__(8) uint64_t full[STG];
     const int tid = threadIdx.x;
     const int lane = tid % g.gv, rph = tid / g.gv;
     const int64_t c0 = (int64_t)lane * V;
@@ -565,18 +572,19 @@ __global__ void __launch_bounds__(kBnThreads, 2) k_bn_tma(
     auto issue = [&](int i) {
         const int64_t rs = r0 + (int64_t)i * tile_rows;
         const uint32_t bytes = (uint32_t)(min((int64_t)tile_rows, r1 - rs) * g.C * (int64_t)sizeof(T));
-        const int st = i % kTmaStages;
+        const int st = i % STG;
         unsigned char* slot = smem + (size_t)st * NIN * kTmaTileBytes;
         mbar_expect_tx(&full[st], bytes * NIN);
         bulk_load(slot, x + rs * g.C, bytes, &full[st]);
         int k = 1;
         if (KIND == 1 || KIND == 3) bulk_load(slot + (k++) * kTmaTileBytes, dy + rs * g.C, bytes, &full[st]);
+        if (DY2) bulk_load(slot + (k++) * kTmaTileBytes, dy2 + rs * g.C, bytes, &full[st]);
         if (RES) bulk_load(slot + k * kTmaTileBytes, res + rs * g.C, bytes, &full[st]);
     };
     if (tid == 0) {
-        for (int st = 0; st < kTmaStages; ++st) mbar_init(&full[st], 1);
+        for (int st = 0; st < STG; ++st) mbar_init(&full[st], 1);
         mbar_init_fence();
-        for (int i = 0; i < min(kTmaStages, n_tiles); ++i) issue(i);
+        for (int i = 0; i < min(STG, n_tiles); ++i) issue(i);
     }
 
     // per-channel state in registers
@@ -605,10 +613,10 @@ __global__ void __launch_bounds__(kBnThreads, 2) k_bn_tma(
     __syncthreads();  // barriers initialised
 
     for (int i = 0; i < n_tiles; ++i) {
-        const int st = i % kTmaStages;
+        const int st = i % STG;
         const int64_t rs = r0 + (int64_t)i * tile_rows;
         const int nr = (int)min((int64_t)tile_rows, r1 - rs);
-        mbar_wait(&full[st], (uint32_t)((i / kTmaStages) & 1));
+        mbar_wait(&full[st], (uint32_t)((i / STG) & 1));
         const T* xs = reinterpret_cast<const T*>(smem + (size_t)st * NIN * kTmaTileBytes);
         const T* ds = reinterpret_cast<const T*>(smem + ((size_t)st * NIN + 1) * kTmaTileBytes);
         const T* rsm = reinterpret_cast<const T*>(smem + ((size_t)st * NIN + NIN - 1) * kTmaTileBytes);
@@ -619,6 +627,12 @@ __global__ void __launch_bounds__(kBnThreads, 2) k_bn_tma(
                 float xv[V], dv[V], rv[V];
                 BnIO<T, V>::load(xs + o, xv);
                 if (KIND == 1 || KIND == 3) BnIO<T, V>::load(ds + o, dv);
+                if (DY2) {
+                    float d2[V];
+                    BnIO<T, V>::load(ds + (size_t)kTmaTileBytes / sizeof(T) + o, d2);
+#pragma unroll
+                    for (int e = 0; e < V; ++e) dv[e] += d2[e];
+                }
                 if (RES) BnIO<T, V>::load(rsm + o, rv);
                 if ((KIND == 1 || KIND == 3) && RELU) {
 #pragma unroll
@@ -657,7 +671,7 @@ __global__ void __launch_bounds__(kBnThreads, 2) k_bn_tma(
             }
         }
         __syncthreads();  // stage st consumed by every thread
-        if (tid == 0 && i + kTmaStages < n_tiles) issue(i + kTmaStages);
+        if (tid == 0 && i + STG < n_tiles) issue(i + STG);
     }
 
     if (KIND == 0 || KIND == 1) {
@@ -821,16 +835,16 @@ static int tma_tile_rows(const BnGeom& g, int elem_bytes) {
 
 // Geometry of the TMA path: one channel group, CTAs = min(resident CTAs, tiles), each CTA a
 // contiguous run of whole tiles.
-template <typename T, int V, int KIND, bool RELU, bool RES>
+template <typename T, int V, int KIND, bool RELU, bool RES, bool DY2 = false>
 static cudaError_t launch_tma(const T* X, const T* DY, const T* R, T* OUT, T* DR, const float* w, const float* b,
                               const float* mean, const float* invstd, const float* coef, float2* part,
-                              BnGeom& g, cudaStream_t s) {
+                              BnGeom& g, cudaStream_t s, const T* DY2p = nullptr) {
   if constexpr (V == 1) {
     return cudaErrorInvalidValue;  // never taken: tma_ok() requires 16-byte vectors
   } else {
-    auto k = k_bn_tma<T, V, KIND, RELU, RES>;
-    constexpr int NIN = tma_inputs<KIND, RES>();
-    const size_t smem = (size_t)kTmaStages * NIN * kTmaTileBytes;
+    auto k = k_bn_tma<T, V, KIND, RELU, RES, DY2>;
+    constexpr int NIN = tma_inputs<KIND, RES, DY2>();
+    const size_t smem = (size_t)tma_stages(NIN) * NIN * kTmaTileBytes;
     static int per_sm = 0;  // one static per template instance
     if (per_sm == 0) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -856,7 +870,7 @@ static cudaError_t launch_tma(const T* X, const T* DY, const T* R, T* OUT, T* DR
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k, X, DY, R, OUT, DR, w, b, mean, invstd, coef, part, g, tr);
+    return cudaLaunchKernelEx(&cfg, k, X, DY, R, OUT, DR, w, b, mean, invstd, coef, part, g, tr, DY2p);
   }
 }
 
@@ -999,7 +1013,8 @@ static int bn_forward_t(const void* x, const void* res, void* y, int64_t rows, i
 }
 
 template <typename T, int V>
-static int bn_backward_t(const void* x, const void* res, const void* dy, void* dx, void* dres, int64_t rows, int64_t C,
+static int bn_backward_t(const void* x, const void* res, const void* dy, const void* dy2, void* dx, void* dres,
+                         int64_t rows, int64_t C,
                          const float* w, const float* b, const float* smean, const float* sinv, int relu, float* dw,
                          float* db, void* ws, cudaStream_t s) {
     const T* X = static_cast<const T*>(x);
@@ -1014,7 +1029,7 @@ static int bn_backward_t(const void* x, const void* res, const void* dy, void* d
     const bool tma = tma_ok(C, V);
     T* DX = static_cast<T*>(dx);
     T* DR = static_cast<T*>(dres);
-    if (tma && fused_mode() && rows * C * (int64_t)sizeof(T) * (2 + (res ? 1 : 0)) <= fused_max_bytes()) {
+    if (!dy2 && tma && fused_mode() && rows * C * (int64_t)sizeof(T) * (2 + (res ? 1 : 0)) <= fused_max_bytes()) {
         if (relu && res)
             e = fused_bwd<T, V, true, true>(X, DY, R, DX, DR, w, b, smean, sinv, dw, db, coef, part, g, s);
         else if (relu)
@@ -1024,7 +1039,11 @@ static int bn_backward_t(const void* x, const void* res, const void* dy, void* d
         MBS_CK(e);
         return MBS_OK;
     }
-    if (tma && relu && res)
+    if (dy2 && !(tma && relu && res)) return invalid("mbs_bn_backward: dy2 needs the fused residual TMA path");
+    if (dy2)
+        e = launch_tma<T, V, 1, true, true, true>(X, DY, R, nullptr, static_cast<T*>(dres), w, b, smean, sinv,
+                                                  nullptr, part, g, s, static_cast<const T*>(dy2));
+    else if (tma && relu && res)
         e = launch_tma<T, V, 1, true, true>(X, DY, R, nullptr, static_cast<T*>(dres), w, b, smean, sinv, nullptr,
                                             part, g, s);   // also writes g = d_residual
     else if (tma && relu)
@@ -1104,25 +1123,26 @@ int mbs_bn_forward(const void* x, const void* residual, void* y, int dtype, int6
     return invalid("mbs_bn_forward: dtype must be MBS_BF16 or MBS_F32");
 }
 
-int mbs_bn_backward(const void* x, const void* residual, const void* dy, void* dx, void* dresidual, int dtype,
-                    int64_t rows, int64_t C, const float* weight, const float* bias, const float* save_mean,
-                    const float* save_invstd, int relu, float* dweight, float* dbias, void* workspace, void* stream) {
+int mbs_bn_backward(const void* x, const void* residual, const void* dy, const void* dy2, void* dx, void* dresidual,
+                    int dtype, int64_t rows, int64_t C, const float* weight, const float* bias,
+                    const float* save_mean, const float* save_invstd, int relu, float* dweight, float* dbias,
+                    void* workspace, void* stream) {
     if (!x || !dy || !dx || !save_mean || !save_invstd || !workspace) return invalid("mbs_bn_backward: null pointer");
     if (rows < 1 || C < 1) return invalid("mbs_bn_backward: rows and C must be >= 1");
     if (!!residual != !!dresidual) return invalid("mbs_bn_backward: residual and dresidual go together");
     if (residual && !relu) return invalid("mbs_bn_backward: a residual is only fused together with the ReLU");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const void* ptrs[5] = {x, residual, dy, dx, dresidual};
-    const int V = dtype == MBS_BF16 || dtype == MBS_F32 ? bn_vec(dtype, C, ptrs, 5) : 0;
+    const void* ptrs[6] = {x, residual, dy, dx, dresidual, dy2};
+    const int V = dtype == MBS_BF16 || dtype == MBS_F32 ? bn_vec(dtype, C, ptrs, 6) : 0;
     if (dtype == MBS_BF16)
-        return V == 8 ? bn_backward_t<__nv_bfloat16, 8>(x, residual, dy, dx, dresidual, rows, C, weight, bias,
+        return V == 8 ? bn_backward_t<__nv_bfloat16, 8>(x, residual, dy, dy2, dx, dresidual, rows, C, weight, bias,
                                                         save_mean, save_invstd, relu, dweight, dbias, workspace, s)
-                      : bn_backward_t<__nv_bfloat16, 1>(x, residual, dy, dx, dresidual, rows, C, weight, bias,
+                      : bn_backward_t<__nv_bfloat16, 1>(x, residual, dy, dy2, dx, dresidual, rows, C, weight, bias,
                                                         save_mean, save_invstd, relu, dweight, dbias, workspace, s);
     if (dtype == MBS_F32)
-        return V == 4 ? bn_backward_t<float, 4>(x, residual, dy, dx, dresidual, rows, C, weight, bias, save_mean,
+        return V == 4 ? bn_backward_t<float, 4>(x, residual, dy, dy2, dx, dresidual, rows, C, weight, bias, save_mean,
                                                 save_invstd, relu, dweight, dbias, workspace, s)
-                      : bn_backward_t<float, 1>(x, residual, dy, dx, dresidual, rows, C, weight, bias, save_mean,
+                      : bn_backward_t<float, 1>(x, residual, dy, dy2, dx, dresidual, rows, C, weight, bias, save_mean,
                                                 save_invstd, relu, dweight, dbias, workspace, s);
     return invalid("mbs_bn_backward: dtype must be MBS_BF16 or MBS_F32");
 }

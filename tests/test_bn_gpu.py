@@ -225,3 +225,79 @@ def test_k5_cooperative_path_matches_three_kernel_path(cuda, shape, mode, monkey
         if a[k] is None:
             continue
         assert rel_l2(a[k].double().cpu().numpy(), c[k].double().cpu().numpy()) <= 1e-6, k
+
+
+def _run_dual(x, res, g1, g2, w, b, relu):
+    xx = x.detach().clone().requires_grad_(True)
+    rr = None if res is None else res.detach().clone().requires_grad_(True)
+    ww = w.detach().clone().requires_grad_(True)
+    bb = b.detach().clone().requires_grad_(True)
+    y1, y2 = K5.micro_batch_norm(xx, ww, bb, relu=relu, residual=rr, dual=True)
+    outs, grads = zip(*[(y, g) for y, g in ((y1, g1), (y2, g2)) if g is not None])
+    torch.autograd.backward(list(outs), list(grads))
+    return dict(y=y1.detach(), dx=xx.grad, dres=None if rr is None else rr.grad, dw=ww.grad, db=bb.grad)
+
+
+@pytest.mark.parametrize("shape", [(8, 64, 14, 14), (4, 256, 7, 9), (2, 2048, 3, 3), (3, 24, 5, 5), (4, 3, 5, 5)])
+@pytest.mark.parametrize("mode", ["relu_res", "relu", "plain"])
+def test_k5_dual_output_fp32_bit_identical_to_summed_gradient(cuda, shape, mode):
+    """Dual output (two consumers of one activation): K5 sums the two gradients in fp32 inside its
+    backward reduce (mbs_bn_backward dy2) — in fp32 that is exactly torch's add, so every output is
+    bit-identical to feeding dy1 + dy2 (C=3: unaligned vectors, Python-side add)."""
+    relu, use_res = mode != "plain", mode == "relu_res"
+    x, res, g1, w, b = _data(cuda, shape, torch.float32, seed=31)
+    g2 = torch.randn_like(g1)
+    res = res if use_res else None
+    a = _run_dual(x, res, g1, g2, w, b, relu)
+    c = _run(x, res, g1 + g2, w, b, relu)
+    for k in a:
+        if a[k] is not None:
+            assert torch.equal(a[k], c[k]), k
+    a = _run_dual(x, res, None, g2, w, b, relu)            # one handle unused: its gradient is None
+    c = _run(x, res, g2, w, b, relu)
+    for k in a:
+        if a[k] is not None:
+            assert torch.equal(a[k], c[k]), k
+
+
+@pytest.mark.parametrize("shape", [(32, 256, 28, 28), (8, 2048, 7, 7)])
+def test_k5_dual_output_bf16_no_worse_than_rounded_add(cuda, shape):
+    """bf16: the in-kernel fp32 sum skips the bf16 rounding of autograd's add — as accurate or better
+    against float64."""
+    x, res, g1, w, b = _data(cuda, shape, torch.bfloat16, seed=32)
+    g2 = torch.randn_like(g1)
+    a = _run_dual(x, res, g1, g2, w, b, True)
+    c = _run(x, res, g1 + g2, w, b, True)
+    ref = _ref64(x, res, w, b, True, g1.double() + g2.double())
+    for k in ("dx", "dres", "dw", "db"):
+        ours = rel_l2(a[k].double().cpu().numpy(), ref[k].double().cpu().numpy())
+        add = rel_l2(c[k].double().cpu().numpy(), ref[k].double().cpu().numpy())
+        assert ours <= max(1e-5, 1.05 * add), (k, ours, add)
+
+
+@pytest.mark.parametrize("arch", ["resnet18", "resnet50"])
+def test_fused_resnet_dual_handles_match_autograd_adds(cuda, arch, monkeypatch):
+    """FusedResNet (block outputs handed on as two handles) vs the same fused model with autograd's
+    adds (MBS_K5_DUAL=0): fp32, deterministic cuDNN — identical outputs, gradients and buffers."""
+    import torchvision
+    monkeypatch.setattr(torch.backends.cudnn, "deterministic", True)
+    monkeypatch.setattr(torch.backends.cudnn, "benchmark", False)
+    torch.manual_seed(0)
+    net = getattr(torchvision.models, arch)(num_classes=10).to(cuda).to(memory_format=torch.channels_last).train()
+    monkeypatch.setenv("MBS_K5_DUAL", "1")
+    dual = K5.fuse_batchnorm(copy.deepcopy(net))
+    monkeypatch.setenv("MBS_K5_DUAL", "0")
+    plain = K5.fuse_batchnorm(copy.deepcopy(net))
+    assert type(dual) is K5.FusedResNet and type(plain) is not K5.FusedResNet
+    assert list(dual.state_dict()) == list(net.state_dict())
+    x = torch.randn(6, 3, 64, 64, device=cuda).contiguous(memory_format=torch.channels_last)
+    outs = []
+    for m in (dual, plain):
+        out = m(x)
+        (out ** 2).mean().backward()
+        outs.append((out.detach(), [p.grad for p in m.parameters()], [v for v in m.state_dict().values()]))
+    assert torch.equal(outs[0][0], outs[1][0])
+    for a, c in zip(outs[0][1], outs[1][1]):
+        assert torch.equal(a, c)
+    for a, c in zip(outs[0][2], outs[1][2]):
+        assert torch.equal(a, c)
