@@ -35,12 +35,17 @@ constexpr int kColTileBytes = 16384;
 // input elements of kernel row kh for output pixel m0+i (consecutive threads take consecutive
 // pixels of the same kernel row, so their global reads are neighbours); padding columns are zeroed.
 // 32-bit index math (the host checks every offset fits).
-template <typename T>
+// KS, CS > 0: kernel size and channel count are compile-time (the ResNet stem's 7x7x3): a work item's
+// k*C loads unroll and are all in flight at once (the runtime loop kept one load per thread in
+// flight: 1.8 TB/s).
+template <typename T, int KS = 0, int CS = 0>
 __global__ void __launch_bounds__(256) k_im2col(const T* __restrict__ x, T* __restrict__ cols, ColGeom g0, int TM) {
     extern __shared__ __align__(16) unsigned char csm[];
     T* tile = reinterpret_cast<T*>(csm);
-    const int H = (int)g0.H, W = (int)g0.W, C = (int)g0.C, Ho = (int)g0.Ho, Wo = (int)g0.Wo, Kp = (int)g0.Kp;
-    const int k = g0.k, s = g0.s, p = g0.p;
+    const int H = (int)g0.H, W = (int)g0.W, Ho = (int)g0.Ho, Wo = (int)g0.Wo, Kp = (int)g0.Kp;
+    const int C = CS > 0 ? CS : (int)g0.C;
+    const int k = KS > 0 ? KS : g0.k;
+    const int s = g0.s, p = g0.p;
     const int KC = k * C, K = k * KC;
     const int64_t M = g0.N * g0.Ho * g0.Wo;
     const int64_t n_tiles = (M + TM - 1) / TM;
@@ -57,13 +62,27 @@ __global__ void __launch_bounds__(256) k_im2col(const T* __restrict__ x, T* __re
             const int ih = oh * s - p + kh, iw0 = ow * s - p;
             T* d = tile + i * Kp + kh * KC;
             if (ih < 0 || ih >= H) {
+#pragma unroll
                 for (int j = 0; j < KC; ++j) d[j] = T(0.f);
             } else {
                 const T* src = x + ((size_t)(n * H + ih) * W) * C;
-                for (int kw = 0; kw < k; ++kw) {
-                    const int iw = iw0 + kw;
-                    const bool in = iw >= 0 && iw < W;
-                    for (int c = 0; c < C; ++c) d[kw * C + c] = in ? src[iw * C + c] : T(0.f);
+                if constexpr (KS > 0 && CS > 0) {
+                    T v[KS * CS];
+#pragma unroll
+                    for (int kw = 0; kw < KS; ++kw) {
+                        const int iw = iw0 + kw;
+                        const bool in = iw >= 0 && iw < W;
+#pragma unroll
+                        for (int c = 0; c < CS; ++c) v[kw * CS + c] = in ? src[iw * CS + c] : T(0.f);
+                    }
+#pragma unroll
+                    for (int j = 0; j < KS * CS; ++j) d[j] = v[j];
+                } else {
+                    for (int kw = 0; kw < k; ++kw) {
+                        const int iw = iw0 + kw;
+                        const bool in = iw >= 0 && iw < W;
+                        for (int c = 0; c < C; ++c) d[kw * C + c] = in ? src[iw * C + c] : T(0.f);
+                    }
                 }
             }
             if (kh == 0)
@@ -124,9 +143,9 @@ int mbs_im2col(const void* x, void* cols, int dtype, int64_t N, int64_t H, int64
     cfg.numAttrs = 1;
     cudaError_t e;
     if (dtype == MBS_BF16) {
-        if (smem > 48 * 1024) cudaFuncSetAttribute(k_im2col<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)smem);
-        e = cudaLaunchKernelEx(&cfg, k_im2col<__nv_bfloat16>, (const __nv_bfloat16*)x, (__nv_bfloat16*)cols, g, TM);
+        auto kern = (k == 7 && C == 3) ? k_im2col<__nv_bfloat16, 7, 3> : k_im2col<__nv_bfloat16>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaLaunchKernelEx(&cfg, kern, (const __nv_bfloat16*)x, (__nv_bfloat16*)cols, g, TM);
     } else {
         if (smem > 48 * 1024) cudaFuncSetAttribute(k_im2col<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         e = cudaLaunchKernelEx(&cfg, k_im2col<float>, (const float*)x, (float*)cols, g, TM);

@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "mbs_common.h"
 
@@ -68,15 +69,43 @@ struct PoolGeom {
 
 // Index math runs in 32 bits whenever every element offset fits (the 64-bit divisions of the
 // grid-stride decomposition dominated these memory-bound kernels: ncu, tools/k6_ncu.py).
+// Division by a runtime-constant divisor: with 32-bit indices (every dividend < 2^31) a multiply-high
+// and a shift, m = ceil(2^(31+l) / d), l = ceil(log2 d) — the pixel decomposition's five divisions
+// were most of the instructions of these instruction-bound kernels (ncu, tools/k6_ncu.py).
+template <typename I>
+struct Div {
+    I d;
+    uint32_t m;
+    int sh;
+    __device__ __forceinline__ I div(I n) const {
+        if constexpr (sizeof(I) == 4) return d == 1 ? n : (I)(__umulhi((uint32_t)n, m) >> sh);
+        else return n / d;
+    }
+};
+
+template <typename I>
+static Div<I> make_div(int64_t d) {
+    Div<I> r{(I)d, 0u, 0};
+    if (sizeof(I) == 4 && d > 1) {
+        int l = 0;
+        while ((1LL << l) < d) ++l;
+        r.m = (uint32_t)(((1ULL << (31 + l)) + (uint64_t)d - 1) / (uint64_t)d);
+        r.sh = l - 1;
+    }
+    return r;
+}
+
 template <typename I>
 struct PoolGeomT {
     I N, H, W, C, Ho, Wo;
     int k, s, p;
+    Div<I> cv, dW, dH, dWo, dHo;   // C / V (the vector width of the launched kernel), W, H, Wo, Ho
 };
 
 template <typename I>
-static PoolGeomT<I> narrow(const PoolGeom& g) {
-    return PoolGeomT<I>{(I)g.N, (I)g.H, (I)g.W, (I)g.C, (I)g.Ho, (I)g.Wo, g.k, g.s, g.p};
+static PoolGeomT<I> narrow(const PoolGeom& g, int V) {
+    return PoolGeomT<I>{(I)g.N, (I)g.H, (I)g.W, (I)g.C, (I)g.Ho, (I)g.Wo, g.k, g.s, g.p, make_div<I>(g.C / V),
+                        make_div<I>(g.W), make_div<I>(g.H), make_div<I>(g.Wo), make_div<I>(g.Ho)};
 }
 
 template <int V>
@@ -115,20 +144,24 @@ __device__ __forceinline__ void load_idx(const uint8_t* p, uint8_t (&v)[V]) {
 // k | H, k | W) every input element is read exactly once, so the kernel also writes it into channel
 // columns [sc0, sc0 + C) of a wider channels-last tensor with row stride sC — the U-Net skip
 // connection lands in its concat buffer without a separate torch.cat pass.
-template <typename T, int V, typename I>
+// K > 0: the window size is a compile-time constant (the ResNet stem's 3x3): the window loops unroll
+// and all k*k loads are in flight at once instead of one per loop trip (no stash on this variant).
+template <typename T, int V, typename I, int K = 0>
 __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restrict__ x, T* __restrict__ y,
                                                               uint8_t* __restrict__ idx, PoolGeomT<I> g,
                                                               T* __restrict__ stash, I sC, I sc0) {
+    const int kk = K > 0 ? K : g.k;
     cudaGridDependencySynchronize();
     const I cv = g.C / V;
     const I total = g.N * g.Ho * g.Wo * cv;
     for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
-        const I c0 = (t % cv) * V;
-        I q = t / cv;
-        const I ow = q % g.Wo;
-        q /= g.Wo;
-        const I oh = q % g.Ho;
-        const I n = q / g.Ho;
+        I q = g.cv.div(t);
+        const I c0 = (t - q * cv) * V;
+        I q2 = g.dWo.div(q);
+        const I ow = q - q2 * g.Wo;
+        q = g.dHo.div(q2);
+        const I oh = q2 - q * g.Ho;
+        const I n = q;
         const I h0 = oh * g.s - g.p, w0 = ow * g.s - g.p;
         float m[V];
         uint8_t a[V];
@@ -137,17 +170,46 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restric
             m[i] = -INFINITY;
             a[i] = 0;
         }
-        for (int kh = 0; kh < g.k; ++kh) {
+        if constexpr (K > 0) {
+            // every in-bounds window element loaded first (k*k loads in flight), then the scan in
+            // torch's order
+            // raw 16-byte words (unpacked only in the scan), out-of-bounds elements load a valid
+            // address unconditionally and are skipped by the scan
+            static_assert(sizeof(T) * V == 16, "the compile-time-window variant takes 16-byte channel vectors");
+            uint4 raw[K * K];
+            bool ok[K * K];
+#pragma unroll
+            for (int q2 = 0; q2 < K * K; ++q2) {
+                const I ih = h0 + q2 / K, iw = w0 + q2 % K;
+                ok[q2] = ih >= 0 && ih < g.H && iw >= 0 && iw < g.W;
+                const I pix = ok[q2] ? (n * g.H + ih) * g.W + iw : (I)0;
+                raw[q2] = __ldg(reinterpret_cast<const uint4*>(x + pix * g.C + c0));
+            }
+#pragma unroll
+            for (int q2 = 0; q2 < K * K; ++q2) {
+                if (!ok[q2]) continue;
+                float v[V];
+                PoolIO<T, V>::load(reinterpret_cast<const T*>(&raw[q2]), v);
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    if (v[i] > m[i] || isnan(v[i])) {
+                        m[i] = v[i];
+                        a[i] = (uint8_t)q2;
+                    }
+                }
+            }
+        } else
+        for (int kh = 0; kh < kk; ++kh) {
             const I ih = h0 + kh;
             if (ih < 0 || ih >= g.H) continue;
-            for (int kw = 0; kw < g.k; ++kw) {
+            for (int kw = 0; kw < kk; ++kw) {
                 const I iw = w0 + kw;
                 if (iw < 0 || iw >= g.W) continue;
                 float v[V];
                 const I pix = (n * g.H + ih) * g.W + iw;
                 PoolIO<T, V>::load(x + pix * g.C + c0, v);
-                if (stash) PoolIO<T, V>::store(stash + pix * sC + sc0 + c0, v);
-                const uint8_t pos = (uint8_t)(kh * g.k + kw);
+                if (K == 0 && stash) PoolIO<T, V>::store(stash + pix * sC + sc0 + c0, v);
+                const uint8_t pos = (uint8_t)(kh * kk + kw);
 #pragma unroll
                 for (int i = 0; i < V; ++i) {
                     if (v[i] > m[i] || isnan(v[i])) {
@@ -166,8 +228,10 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restric
 // Optional addend: dx += add[pixel, ac0 + c] (row stride aC) in fp32 before the single rounding —
 // the gradient that reached the same tensor through the U-Net skip connection, fused instead of
 // autograd's separate add pass.
-// W2: non-overlapping windows tiling the input (the U-Net 2x2/s2 pools) — no window search.
-template <typename T, int V, typename I, bool W2>
+// W2 = 1: non-overlapping windows tiling the input (the U-Net 2x2/s2 pools) — no window search.
+// W2 = 2: 3x3 windows, stride 2 (the ResNet stem): at most 2x2 candidate windows, unrolled and
+// predicated so their index/gradient loads are all in flight at once.
+template <typename T, int V, typename I, int W2>
 __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restrict__ dy,
                                                               const uint8_t* __restrict__ idx, T* __restrict__ dx,
                                                               PoolGeomT<I> g, const T* __restrict__ add, I aC,
@@ -176,24 +240,55 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
     const I cv = g.C / V;
     const I total = g.N * g.H * g.W * cv;
     for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
-        const I c0 = (t % cv) * V;
-        I q = t / cv;
-        const I iw = q % g.W;
-        q /= g.W;
-        const I ih = q % g.H;
-        const I n = q / g.H;
+        I q = g.cv.div(t);
+        const I c0 = (t - q * cv) * V;
+        I q2 = g.dW.div(q);
+        const I iw = q - q2 * g.W;
+        q = g.dH.div(q2);
+        const I ih = q2 - q * g.H;
+        const I n = q;
         const I pix = (n * g.H + ih) * g.W + iw;
         float a2[V];
         if (add) PoolIO<T, V>::load(add + pix * aC + ac0 + c0, a2);   // independent of the windows: issue first
         // windows containing (ih, iw): oh*s - p <= ih <= oh*s - p + k - 1
-        const I ohs = max((I)0, (ih + g.p - g.k + g.s) / g.s);
-        const I ohe = min(g.Ho, (ih + g.p) / g.s + 1);
-        const I ows = max((I)0, (iw + g.p - g.k + g.s) / g.s);
-        const I owe = min(g.Wo, (iw + g.p) / g.s + 1);
+        const int sk = W2 == 2 ? 2 : g.s, kk = W2 == 2 ? 3 : g.k;   // 3x3/s2: constant divisions
+        const I ohs = max((I)0, (ih + g.p - kk + sk) / sk);
+        const I ohe = min(g.Ho, (ih + g.p) / sk + 1);
+        const I ows = max((I)0, (iw + g.p - kk + sk) / sk);
+        const I owe = min(g.Wo, (iw + g.p) / sk + 1);
         float acc[V];
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[i] = 0.f;
-        if constexpr (W2) {
+        if constexpr (W2 == 2 && sizeof(T) * V == 16) {
+            // all four candidate windows' idx / dy loaded first (out-of-range ones from a valid
+            // address, skipped below), then summed in ascending (oh, ow) order
+            using IRaw = typename std::conditional<V == 8, uint2, uint32_t>::type;
+            uint4 draw[4];
+            IRaw iraw[4];
+            bool ok[4];
+            uint8_t pos[4];
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+                const I oh = ohs + q2 / 2, ow = ows + q2 % 2;
+                const int kh = (int)(ih - (oh * 2 - g.p)), kw = (int)(iw - (ow * 2 - g.p));
+                ok[q2] = oh < ohe && ow < owe && kh >= 0 && kh < 3 && kw >= 0 && kw < 3;
+                pos[q2] = (uint8_t)(kh * 3 + kw);
+                const I o = ok[q2] ? ((n * g.Ho + oh) * g.Wo + ow) * g.C + c0 : (I)0;
+                iraw[q2] = __ldg(reinterpret_cast<const IRaw*>(idx + o));
+                draw[q2] = __ldg(reinterpret_cast<const uint4*>(dy + o));
+            }
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+                if (!ok[q2]) continue;
+                uint8_t a[V];
+                float d[V];
+                load_idx<V>(reinterpret_cast<const uint8_t*>(&iraw[q2]), a);
+                PoolIO<T, V>::load(reinterpret_cast<const T*>(&draw[q2]), d);
+#pragma unroll
+                for (int i = 0; i < V; ++i)
+                    if (a[i] == pos[q2]) acc[i] += d[i];
+            }
+        } else if constexpr (W2 == 1) {
             // non-overlapping windows (k == s, p == 0): exactly one window per input element
             const I oh = ih / g.s, ow = iw / g.s;
             const uint8_t pos = (uint8_t)((ih - oh * g.s) * g.k + (iw - ow * g.s));
@@ -292,8 +387,13 @@ static cudaError_t pool_launch(void (*kernel)(KArgs...), int64_t work, cudaStrea
         cudaGetDevice(&dev);
         if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
     }
+    // one full wave: resident CTAs per SM from the occupancy calculator (a 2nd partial wave of a
+    // grid-stride loop costs a whole CTA lifetime)
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kPoolThreads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
     const int64_t want = (work + kPoolThreads - 1) / kPoolThreads;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, 8LL * sms));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)std::min(per_sm, 8) * sms));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kPoolThreads);
@@ -326,7 +426,7 @@ static bool fits_i32(int64_t v) { return v < (int64_t)INT32_MAX - (1 << 22); }  
 template <typename I>
 static int maxpool_fwd(const void* x, void* y, uint8_t* idx, int dtype, const PoolGeom& g0, void* stash, int64_t sC,
                        int64_t sc0, cudaStream_t cs) {
-    const PoolGeomT<I> g = narrow<I>(g0);
+    const PoolGeomT<I> gv = narrow<I>(g0, dtype == MBS_BF16 ? 8 : 4), g1 = narrow<I>(g0, 1);
     const int64_t outs = g0.N * g0.Ho * g0.Wo;
     const int es = dtype == MBS_BF16 ? 2 : 4;
     const bool stash_vec = !stash || (!(reinterpret_cast<uintptr_t>(stash) & 15) && (sC * es) % 16 == 0 &&
@@ -336,26 +436,29 @@ static int maxpool_fwd(const void* x, void* y, uint8_t* idx, int dtype, const Po
     if (dtype == MBS_BF16) {
         using T = __nv_bfloat16;
         if (g0.C % 8 == 0 && aligned16(x, y, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7) && stash_vec)
-            e = pool_launch(k_maxpool_fwd<T, 8, I>, outs * (g0.C / 8), cs, (const T*)x, (T*)y, idx, g, (T*)stash, isC,
-                            isc0);
+            e = (g0.k == 3 && !stash)
+                    ? pool_launch(k_maxpool_fwd<T, 8, I, 3>, outs * (g0.C / 8), cs, (const T*)x, (T*)y, idx, gv,
+                                  (T*)nullptr, isC, isc0)
+                    : pool_launch(k_maxpool_fwd<T, 8, I>, outs * (g0.C / 8), cs, (const T*)x, (T*)y, idx, gv,
+                                  (T*)stash, isC, isc0);
         else
-            e = pool_launch(k_maxpool_fwd<T, 1, I>, outs * g0.C, cs, (const T*)x, (T*)y, idx, g, (T*)stash, isC, isc0);
+            e = pool_launch(k_maxpool_fwd<T, 1, I>, outs * g0.C, cs, (const T*)x, (T*)y, idx, g1, (T*)stash, isC, isc0);
     } else {
         if (g0.C % 4 == 0 && aligned16(x, y, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 3) && stash_vec)
-            e = pool_launch(k_maxpool_fwd<float, 4, I>, outs * (g0.C / 4), cs, (const float*)x, (float*)y, idx, g,
+            e = pool_launch(k_maxpool_fwd<float, 4, I>, outs * (g0.C / 4), cs, (const float*)x, (float*)y, idx, gv,
                             (float*)stash, isC, isc0);
         else
-            e = pool_launch(k_maxpool_fwd<float, 1, I>, outs * g0.C, cs, (const float*)x, (float*)y, idx, g,
+            e = pool_launch(k_maxpool_fwd<float, 1, I>, outs * g0.C, cs, (const float*)x, (float*)y, idx, g1,
                             (float*)stash, isC, isc0);
     }
     MBS_CK(e);
     return MBS_OK;
 }
 
-template <typename I, bool W2>
+template <typename I, int W2>
 static int maxpool_bwd(const void* dy, const uint8_t* idx, void* dx, int dtype, const PoolGeom& g0, const void* add,
                        int64_t aC, int64_t ac0, cudaStream_t cs) {
-    const PoolGeomT<I> g = narrow<I>(g0);
+    const PoolGeomT<I> gv = narrow<I>(g0, dtype == MBS_BF16 ? 8 : 4), g1 = narrow<I>(g0, 1);
     const int64_t ins = g0.N * g0.H * g0.W;
     const int es = dtype == MBS_BF16 ? 2 : 4;
     const bool add_vec = !add || (!(reinterpret_cast<uintptr_t>(add) & 15) && (aC * es) % 16 == 0 &&
@@ -365,17 +468,17 @@ static int maxpool_bwd(const void* dy, const uint8_t* idx, void* dx, int dtype, 
     if (dtype == MBS_BF16) {
         using T = __nv_bfloat16;
         if (g0.C % 8 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7) && add_vec)
-            e = pool_launch(k_maxpool_bwd<T, 8, I, W2>, ins * (g0.C / 8), cs, (const T*)dy, idx, (T*)dx, g, (const T*)add,
+            e = pool_launch(k_maxpool_bwd<T, 8, I, W2>, ins * (g0.C / 8), cs, (const T*)dy, idx, (T*)dx, gv, (const T*)add,
                             iaC, iac0);
         else
-            e = pool_launch(k_maxpool_bwd<T, 1, I, W2>, ins * g0.C, cs, (const T*)dy, idx, (T*)dx, g, (const T*)add, iaC,
+            e = pool_launch(k_maxpool_bwd<T, 1, I, W2>, ins * g0.C, cs, (const T*)dy, idx, (T*)dx, g1, (const T*)add, iaC,
                             iac0);
     } else {
         if (g0.C % 4 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 3) && add_vec)
-            e = pool_launch(k_maxpool_bwd<float, 4, I, W2>, ins * (g0.C / 4), cs, (const float*)dy, idx, (float*)dx, g,
+            e = pool_launch(k_maxpool_bwd<float, 4, I, W2>, ins * (g0.C / 4), cs, (const float*)dy, idx, (float*)dx, gv,
                             (const float*)add, iaC, iac0);
         else
-            e = pool_launch(k_maxpool_bwd<float, 1, I, W2>, ins * g0.C, cs, (const float*)dy, idx, (float*)dx, g,
+            e = pool_launch(k_maxpool_bwd<float, 1, I, W2>, ins * g0.C, cs, (const float*)dy, idx, (float*)dx, g1,
                             (const float*)add, iaC, iac0);
     }
     MBS_CK(e);
@@ -440,11 +543,14 @@ int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype
     const bool i32 = fits_i32(g.N * g.H * g.W * std::max<int64_t>(g.C, addend ? add_C : 0)) &&
                      fits_i32(g.N * g.Ho * g.Wo * g.C);
     const bool w2 = g.k == g.s && g.p == 0 && g.H % g.k == 0 && g.W % g.k == 0;   // one window per element
+    const bool k3s2 = g.k == 3 && g.s == 2 && g.C % (dtype == MBS_BF16 ? 8 : 4) == 0 && aligned16(dy, dx, nullptr) &&
+                      !(reinterpret_cast<uintptr_t>(idx) & (dtype == MBS_BF16 ? 7 : 3));
     if (i32)
-        return w2 ? maxpool_bwd<int32_t, true>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs)
-                  : maxpool_bwd<int32_t, false>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs);
-    return w2 ? maxpool_bwd<int64_t, true>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs)
-              : maxpool_bwd<int64_t, false>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs);
+        return w2     ? maxpool_bwd<int32_t, 1>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs)
+               : k3s2 ? maxpool_bwd<int32_t, 2>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs)
+                      : maxpool_bwd<int32_t, 0>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs);
+    return w2 ? maxpool_bwd<int64_t, 1>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs)
+              : maxpool_bwd<int64_t, 0>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs);
 }
 
 int mbs_copy_channels(const void* src, int64_t src_C, int64_t src_c0, void* dst, int64_t dst_C, int64_t dst_c0,

@@ -13,7 +13,8 @@ from paper_2110_12484_b200 import pool as K6
 pytestmark = pytest.mark.gpu
 
 CASES = [((4, 64, 112, 112), 3, 2, 1), ((3, 64, 48, 48), 2, 2, 0), ((2, 24, 17, 13), 3, 2, 1),
-         ((2, 8, 9, 9), 3, 1, 1), ((2, 5, 11, 7), 2, 2, 0), ((1, 16, 7, 7), 3, 3, 0), ((2, 32, 10, 10), 5, 2, 2)]
+         ((2, 8, 9, 9), 3, 1, 1), ((2, 5, 11, 7), 2, 2, 0), ((1, 16, 7, 7), 3, 3, 0), ((2, 32, 10, 10), 5, 2, 2),
+         ((2, 16, 15, 14), 3, 2, 0), ((2, 8, 8, 9), 3, 2, 1), ((2, 40, 3, 3), 3, 2, 1)]
 
 
 def _pair(x, k, s, p, dy):
