@@ -97,6 +97,83 @@ __global__ void __launch_bounds__(256) k_im2col(const T* __restrict__ x, T* __re
     }
 }
 
+// Row variant (the ResNet stem and U-Net first conv: compile-time k, C, Kp): one CTA per output row
+// (n, oh). Its k input rows are staged once in shared memory with 16-byte coalesced loads (zero
+// columns for the padding), then each thread owns one fixed 16-byte chunk j of the Kp-wide patch
+// row — the 8 (kh, kw, c) sources of that chunk are computed once — and walks the row's output
+// pixels: 8 two-byte shared loads, one 16-byte coalesced global store per pixel. The tile variant
+// above spent its time on 2-byte shared stores and barriers (ncu: L1 91 % busy, 2.1 TB/s).
+template <typename T, int KS, int CS, int KP>
+__global__ void __launch_bounds__(256) k_im2col_rows(const T* __restrict__ x, T* __restrict__ cols, ColGeom g0,
+                                                     int LP, int RS) {
+    constexpr int NCH = KP * (int)sizeof(T) / 16;   // 16-byte chunks per patch row
+    constexpr int EPC = 16 / (int)sizeof(T);        // elements per chunk
+    constexpr int KK = KS * KS * CS;                // real (unpadded) patch length
+    constexpr int ISTEP = 256 / NCH;
+    extern __shared__ __align__(16) unsigned char csm[];
+    T* rows = reinterpret_cast<T*>(csm);
+    const int H = (int)g0.H, W = (int)g0.W, Ho = (int)g0.Ho, Wo = (int)g0.Wo;
+    const int s = g0.s, p = g0.p;
+    const int tid = threadIdx.x;
+    const int j = tid % NCH, i0 = tid / NCH;
+    int off[EPC];
+    bool live[EPC];
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) {
+        const int k = j * EPC + e;
+        const int kh = k / (KS * CS), r = k - kh * (KS * CS);
+        live[e] = k < KK;
+        off[e] = live[e] ? kh * RS + LP - p * CS + r : 0;
+    }
+    const int WC = W * CS;
+    const bool vec = (WC * (int)sizeof(T)) % 16 == 0 && (LP * (int)sizeof(T)) % 16 == 0;
+    cudaGridDependencySynchronize();
+    for (int64_t row = blockIdx.x; row < g0.N * Ho; row += gridDim.x) {
+        const int n = (int)(row / Ho), oh = (int)(row - (int64_t)n * Ho);
+        // stage: k input rows, zero padding columns / rows
+        for (int kh = 0; kh < KS; ++kh) {
+            const int ih = oh * s - p + kh;
+            T* dst = rows + kh * RS;
+            if (ih < 0 || ih >= H) {
+                for (int q = tid; q < RS; q += blockDim.x) dst[q] = T(0.f);
+                continue;
+            }
+            const T* src = x + ((int64_t)n * H + ih) * WC;
+            for (int q = tid; q < LP; q += blockDim.x) dst[q] = T(0.f);
+            for (int q = LP + WC + tid; q < RS; q += blockDim.x) dst[q] = T(0.f);
+            if (vec) {
+                const uint4* s16 = reinterpret_cast<const uint4*>(src);
+                uint4* d16 = reinterpret_cast<uint4*>(dst + LP);
+                for (int q = tid; q < WC * (int)sizeof(T) / 16; q += blockDim.x) d16[q] = __ldg(s16 + q);
+            } else {
+                for (int q = tid; q < WC; q += blockDim.x) dst[LP + q] = src[q];
+            }
+        }
+        __syncthreads();
+        if (i0 < ISTEP) {
+            T* out = cols + row * Wo * KP + j * EPC;
+            for (int i = i0; i < Wo; i += ISTEP) {
+                const int base = i * s * CS;
+                uint16_t v[EPC];
+#pragma unroll
+                for (int e = 0; e < EPC; ++e) {
+                    const T t = live[e] ? rows[base + off[e]] : T(0.f);
+                    v[e] = *reinterpret_cast<const uint16_t*>(&t);
+                }
+                uint4 u;
+                if constexpr (sizeof(T) == 2) {
+                    u.x = v[0] | ((uint32_t)v[1] << 16);
+                    u.y = v[2] | ((uint32_t)v[3] << 16);
+                    u.z = v[4] | ((uint32_t)v[5] << 16);
+                    u.w = v[6] | ((uint32_t)v[7] << 16);
+                }
+                *reinterpret_cast<uint4*>(out + (int64_t)i * KP) = u;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 static int im2col_sms() {
     static int n = 0;
     if (n <= 0) {
@@ -142,6 +219,24 @@ int mbs_im2col(const void* x, void* cols, int dtype, int64_t N, int64_t H, int64
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e;
+    // row variant: bf16, (k, C, Kp) in {(7, 3, 152), (3, 3, 32)}, k input rows fit in shared memory
+    void (*rowk)(const __nv_bfloat16*, __nv_bfloat16*, ColGeom, int, int) = nullptr;
+    if (dtype == MBS_BF16 && C == 3 && k == 7 && Kp == 152) rowk = k_im2col_rows<__nv_bfloat16, 7, 3, 152>;
+    if (dtype == MBS_BF16 && C == 3 && k == 3 && Kp == 32) rowk = k_im2col_rows<__nv_bfloat16, 3, 3, 32>;
+    const int LP = (int)((p * C + 7) / 8 * 8);
+    const int RS = (int)((LP + (W + p) * C + 7) / 8 * 8);
+    const size_t rsmem = (size_t)k * RS * 2;
+    if (rowk && rsmem <= 96 * 1024 && !(reinterpret_cast<uintptr_t>(x) & 15) && N * H * W * C < INT32_MAX / 2) {
+        if (rsmem > 48 * 1024) cudaFuncSetAttribute(rowk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rowk, 256, rsmem) != cudaSuccess || per_sm < 1)
+            per_sm = 1;
+        cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(N * Ho, (int64_t)per_sm * im2col_sms())));
+        cfg.dynamicSmemBytes = rsmem;
+        e = cudaLaunchKernelEx(&cfg, rowk, (const __nv_bfloat16*)x, (__nv_bfloat16*)cols, g, LP, RS);
+        MBS_CK(e);
+        return MBS_OK;
+    }
     if (dtype == MBS_BF16) {
         auto kern = (k == 7 && C == 3) ? k_im2col<__nv_bfloat16, 7, 3> : k_im2col<__nv_bfloat16>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

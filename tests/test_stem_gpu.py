@@ -114,3 +114,27 @@ def test_pointwise_gemm_conv_matches(cuda):
     assert rel_l2(x.grad.double().cpu().numpy(), xr.grad.cpu().numpy()) <= 1e-6
     assert rel_l2(conv.weight.grad.double().cpu().numpy(), ref.weight.grad.cpu().numpy()) <= 1e-6
     assert rel_l2(conv.bias.grad.double().cpu().numpy(), ref.bias.grad.cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("case", [((3, 3, 224, 224), 7, 2, 3), ((2, 3, 37, 29), 7, 2, 3), ((2, 3, 48, 40), 3, 1, 1),
+                                  ((2, 3, 17, 11), 3, 1, 1), ((2, 3, 16, 16), 3, 2, 0), ((2, 3, 15, 15), 5, 1, 2)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_k7_im2col_bit_identical_to_unfold(cuda, case, dtype):
+    """K7's patch matrix is pure data movement: every variant (the staged-row kernels for 7x7x3 / 3x3x3
+    bf16, the tile kernel otherwise; widths whose rows are / are not 16-byte multiples) must equal
+    torch's unfold reordered to (kh, kw, c), zero padding columns included."""
+    from paper_2110_12484_b200 import _native
+    shape, k, s, p = case
+    n, c, h, w = shape
+    x = torch.randn(shape, device=cuda).to(dtype).contiguous(memory_format=torch.channels_last)
+    ho, wo = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    kk = k * k * c
+    kp = (kk + 7) // 8 * 8
+    cols = torch.full((n * ho * wo, kp), float("nan"), device=cuda, dtype=dtype)
+    code = _native.BF16 if dtype == torch.bfloat16 else _native.F32
+    _native.check(_native.lib().mbs_im2col(x.data_ptr(), cols.data_ptr(), code, n, h, w, c, k, s, p, kp,
+                                           torch.cuda.current_stream().cuda_stream), "mbs_im2col")
+    u = F.unfold(x.float(), k, padding=p, stride=s)                  # [n, c*k*k (c, kh, kw), L]
+    ref = u.view(n, c, k, k, ho * wo).permute(0, 4, 2, 3, 1).reshape(n * ho * wo, kk).to(dtype)
+    assert torch.equal(cols[:, :kk], ref)
+    assert torch.equal(cols[:, kk:], torch.zeros_like(cols[:, kk:]))
