@@ -6,6 +6,11 @@ timeout 600 python bench.py --config c3 --no-cpu-baseline > gpurun_out/final_c3.
 timeout 900 python bench.py --config c5 --no-cpu-baseline > gpurun_out/final_c5.json 2> gpurun_out/final_c5.err
 timeout 1500 python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/final_c4.json 2> gpurun_out/final_c4.err
 timeout 400 python bench.py --impl reference > gpurun_out/final_ref.json 2> gpurun_out/final_ref.err
+# launch list + one --set full capture of the MBS step (C2), tag ${TAG:-r01_c2_v7}
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/${TAG:-r01_c2_v7}_launches.csv python tools/profile_step.py > /dev/null 2>&1
+timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none \
+    -k regex:"k_stage|k_accum|k_finalize|k_sgd" -o gpurun_out/${TAG:-r01_c2_v7}_full python tools/profile_step.py > /dev/null 2>&1
 python -c "
 import json
 for f in ['gpurun_out/final_c2.json','gpurun_out/final_c3.json','gpurun_out/final_c5.json','gpurun_out/final_c4.json','gpurun_out/final_ref.json']:
