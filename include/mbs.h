@@ -248,10 +248,12 @@ int mbs_accum_add_allreduce(mbs_accum_t h, mbs_peer_t peer, const float* const* 
  * Deterministic: fixed-order reductions, no atomics.
  * ------------------------------------------------------------------------- */
 int mbs_bn_workspace_bytes(int64_t rows, int64_t C, int dtype, int64_t* bytes);
+/* num_batches_tracked (nullable, device int64): incremented by one on the stream (torch's
+ * BatchNorm2d.num_batches_tracked += 1), so no separate counter kernel runs per layer. */
 int mbs_bn_forward(const void* x, const void* residual, void* y, int dtype, int64_t rows, int64_t C,
                    const float* weight, const float* bias, float* running_mean, float* running_var,
-                   double momentum, double eps, int relu, float* save_mean, float* save_invstd,
-                   void* workspace, void* stream);
+                   int64_t* num_batches_tracked, double momentum, double eps, int relu, float* save_mean,
+                   float* save_invstd, void* workspace, void* stream);
 /* Gradients of mbs_bn_forward: dx, dresidual (iff residual), dweight/dbias (may be NULL).
  * The ReLU mask is recomputed from x (and residual) bit-identically to the forward.
  * dy2 (nullable): a second gradient of y (the output feeds both the next block's main path and its

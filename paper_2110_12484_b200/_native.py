@@ -77,7 +77,8 @@ _SIGS = {
                                         c_double, c_double, c_void_p]),
     "mbs_bn_workspace_bytes": (c_int, [c_int64, c_int64, c_int, POINTER(c_int64)]),
     "mbs_bn_forward": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
-                               c_void_p, c_double, c_double, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
+                               c_void_p, c_void_p, c_double, c_double, c_int, c_void_p, c_void_p, c_void_p,
+                               c_void_p]),
     "mbs_bn_backward": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64,
                                 c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),

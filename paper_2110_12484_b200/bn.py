@@ -94,7 +94,8 @@ class _MicroBatchNormFn(torch.autograd.Function):
     """y = relu?(bn(x) [+ residual]) with micro-batch statistics; one running-stat update."""
 
     @staticmethod
-    def forward(ctx, x, residual, weight, bias, running_mean, running_var, momentum, eps, relu, dual=False):
+    def forward(ctx, x, residual, weight, bias, running_mean, running_var, momentum, eps, relu, dual=False,
+                num_batches_tracked=None):
         code = _DTYPES.get(x.dtype)
         if code is None:
             raise ValueError(f"micro-batch BatchNorm supports bfloat16 / float32 activations, got {x.dtype}")
@@ -115,7 +116,8 @@ class _MicroBatchNormFn(torch.autograd.Function):
         ev = TIMER.start_k5(_n_kernels(C, (x, residual, y), x.numel() * x.element_size()), stream)
         _native.check(_native.lib().mbs_bn_forward(
             _ptr(x), _ptr(residual), _ptr(y), code, rows, C, _ptr(weight), _ptr(bias), _ptr(running_mean),
-            _ptr(running_var), float(momentum), float(eps), int(relu), _ptr(mean), _ptr(invstd), _ptr(ws), st),
+            _ptr(running_var), _ptr(num_batches_tracked), float(momentum), float(eps), int(relu), _ptr(mean),
+            _ptr(invstd), _ptr(ws), st),
             "mbs_bn_forward")
         # algorithmic bytes: stats read x; apply read x (+ residual), write y
         TIMER.stop("k5_bn_forward", ev, x.numel() * x.element_size() * (3 + (residual is not None)), stream)
@@ -158,7 +160,7 @@ class _MicroBatchNormFn(torch.autograd.Function):
         # elemt read x and dy (or g), write dx
         TIMER.stop("k5_bn_backward", ev,
                    x.numel() * x.element_size() * (5 + 2 * ctx.has_res + (dy2 is not None)), stream)
-        return dx, dres, dw, db, None, None, None, None, None, None
+        return dx, dres, dw, db, None, None, None, None, None, None, None
 
 
 def micro_batch_norm(x, weight, bias, running_mean=None, running_var=None, *, momentum=0.1, eps=1e-5,
@@ -202,16 +204,21 @@ class MicroBatchNorm2d(nn.BatchNorm2d):
                                "(libmbs_native.so) and needs a CUDA tensor; there is no CPU fallback")
         momentum = 0.0 if self.momentum is None else self.momentum
         track = self.training and self.track_running_stats
+        nbt = None
         if track:
-            self.num_batches_tracked.add_(1)
-            if self.momentum is None:              # cumulative moving average (torch semantics)
+            if self.momentum is None:              # cumulative moving average (torch semantics): needs the count
+                self.num_batches_tracked.add_(1)
                 momentum = 1.0 / float(self.num_batches_tracked)
+            elif self.num_batches_tracked.dtype == torch.int64 and self.num_batches_tracked.is_cuda:
+                nbt = self.num_batches_tracked     # += 1 inside K5's statistics finalize (no counter kernel)
+            else:
+                self.num_batches_tracked.add_(1)
         if residual is not None and not self.fuse_relu:
             raise ValueError("MicroBatchNorm2d: a residual needs fuse_relu=True")
         return _MicroBatchNormFn.apply(x, residual, self.weight, self.bias,
                                        self.running_mean if track else None,
                                        self.running_var if track else None,
-                                       momentum, self.eps, self.fuse_relu, dual)
+                                       momentum, self.eps, self.fuse_relu, dual, nbt)
 
 
 def _as_micro_bn(bn: nn.BatchNorm2d, relu: bool) -> MicroBatchNorm2d:

@@ -94,6 +94,7 @@ struct BnGeom {
     int rp;            // rows per pass = 256 / gv
     int64_t chunk;     // rows per CTA
     int P;             // CTAs along rows (= partials per channel for the reductions)
+    long long* nbt = nullptr;   // num_batches_tracked, incremented once by the statistics finalize (nullable)
 };
 
 // Per-channel affine of the forward (shared by forward apply and the backward mask
@@ -303,6 +304,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_stats_finalize(
         float* __restrict__ save_mean, float* __restrict__ save_invstd, float* __restrict__ coef) {
     const int64_t c = (int64_t)blockIdx.x * (kBnThreads / TPC) + threadIdx.x / TPC;
     cudaGridDependencySynchronize();  // PDL: partials come from the statistics kernel
+    if (g.nbt && blockIdx.x == 0 && threadIdx.x == 0) *g.nbt += 1;   // torch's num_batches_tracked += 1
     double s1, s2;
     if (group_merge<TPC>(part + c * g.P, g.P, c < g.C, s1, s2))
         bn_stats_write(x, g, w, b, running_mean, running_var, momentum, eps, save_mean, save_invstd, coef, c, s1, s2);
@@ -486,6 +488,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_fused_fwd(
         float2* __restrict__ part, BnGeom g) {
     cg::grid_group grid = cg::this_grid();
     cudaGridDependencySynchronize();
+    if (g.nbt && blockIdx.x == 0 && threadIdx.x == 0) *g.nbt += 1;
     bn_reduce_body<T, V, 0, false, false>(x, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, part, g,
                                           blockIdx.x, 0);
     grid.sync();
@@ -948,9 +951,10 @@ static cudaError_t coop_launch(void (*kernel)(KArgs...), int grid, cudaStream_t 
 template <typename T, int V, bool RELU, bool RES>
 static cudaError_t fused_fwd(const T* X, const T* R, T* Y, const float* w, const float* b, float* rm, float* rv,
                              double momentum, double eps, float* smean, float* sinv, float* coef, float2* part,
-                             BnGeom g, cudaStream_t s) {
+                             BnGeom g, cudaStream_t s, long long* nbt) {
     auto k = k_bn_fused_fwd<T, V, RELU, RES>;
     if (!coop_geometry(k, g, V)) return cudaErrorCooperativeLaunchTooLarge;
+    g.nbt = nbt;
     return coop_launch(k, g.P, s, X, R, Y, w, b, rm, rv, momentum, eps, smean, sinv, coef, part, g);
 }
 
@@ -965,8 +969,8 @@ static cudaError_t fused_bwd(const T* X, const T* DY, const T* R, T* DX, T* DR, 
 
 template <typename T, int V>
 static int bn_forward_t(const void* x, const void* res, void* y, int64_t rows, int64_t C, const float* w,
-                        const float* b, float* rm, float* rv, double momentum, double eps, int relu, float* smean,
-                        float* sinv, void* ws, cudaStream_t s) {
+                        const float* b, float* rm, float* rv, long long* nbt, double momentum, double eps, int relu,
+                        float* smean, float* sinv, void* ws, cudaStream_t s) {
     const T* X = static_cast<const T*>(x);
     const T* R = static_cast<const T*>(res);
     T* Y = static_cast<T*>(y);
@@ -979,11 +983,14 @@ static int bn_forward_t(const void* x, const void* res, void* y, int64_t rows, i
     if (tma && fused_mode() && rows * C * (int64_t)sizeof(T) <= fused_max_bytes()) {
         cudaError_t e;
         if (relu && res)
-            e = fused_fwd<T, V, true, true>(X, R, Y, w, b, rm, rv, momentum, eps, smean, sinv, coef, part, g, s);
+            e = fused_fwd<T, V, true, true>(X, R, Y, w, b, rm, rv, momentum, eps, smean, sinv, coef, part, g, s,
+                                        nbt);
         else if (relu)
-            e = fused_fwd<T, V, true, false>(X, R, Y, w, b, rm, rv, momentum, eps, smean, sinv, coef, part, g, s);
+            e = fused_fwd<T, V, true, false>(X, R, Y, w, b, rm, rv, momentum, eps, smean, sinv, coef, part, g, s,
+                                        nbt);
         else
-            e = fused_fwd<T, V, false, false>(X, R, Y, w, b, rm, rv, momentum, eps, smean, sinv, coef, part, g, s);
+            e = fused_fwd<T, V, false, false>(X, R, Y, w, b, rm, rv, momentum, eps, smean, sinv, coef, part, g, s,
+                                        nbt);
         MBS_CK(e);
         return MBS_OK;
     }
@@ -992,6 +999,7 @@ static int bn_forward_t(const void* x, const void* res, void* y, int64_t rows, i
     MBS_CK((launch_reduce<T, V, 0, false, false>(X, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, part, g,
                                                   s)));
     const int tpc = tpc_for(g.P);
+    g.nbt = nbt;
     cudaError_t e;
     if (tpc == 32) e = launch_stats_finalize<T, 32>(X, part, g, w, b, rm, rv, momentum, eps, smean, sinv, coef, s);
     else if (tpc == 64) e = launch_stats_finalize<T, 64>(X, part, g, w, b, rm, rv, momentum, eps, smean, sinv, coef, s);
@@ -1100,26 +1108,28 @@ int mbs_bn_workspace_bytes(int64_t rows, int64_t C, int dtype, int64_t* bytes) {
 }
 
 int mbs_bn_forward(const void* x, const void* residual, void* y, int dtype, int64_t rows, int64_t C,
-                   const float* weight, const float* bias, float* running_mean, float* running_var, double momentum,
-                   double eps, int relu, float* save_mean, float* save_invstd, void* workspace, void* stream) {
+                   const float* weight, const float* bias, float* running_mean, float* running_var,
+                   int64_t* num_batches_tracked, double momentum, double eps, int relu, float* save_mean,
+                   float* save_invstd, void* workspace, void* stream) {
     if (!x || !y || !save_mean || !save_invstd || !workspace) return invalid("mbs_bn_forward: null pointer");
     if (rows < 1 || C < 1) return invalid("mbs_bn_forward: rows and C must be >= 1");
     if (!!running_mean != !!running_var) return invalid("mbs_bn_forward: running_mean/running_var must both be set");
     if (residual && !relu) return invalid("mbs_bn_forward: a residual is only fused together with the ReLU");
     if (!(eps > 0.0)) return invalid("mbs_bn_forward: eps must be > 0");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    long long* nbt = reinterpret_cast<long long*>(num_batches_tracked);
     const void* ptrs[3] = {x, residual, y};
     const int V = dtype == MBS_BF16 || dtype == MBS_F32 ? bn_vec(dtype, C, ptrs, 3) : 0;
     if (dtype == MBS_BF16)
         return V == 8 ? bn_forward_t<__nv_bfloat16, 8>(x, residual, y, rows, C, weight, bias, running_mean, running_var,
-                                                       momentum, eps, relu, save_mean, save_invstd, workspace, s)
+                                                       nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s)
                       : bn_forward_t<__nv_bfloat16, 1>(x, residual, y, rows, C, weight, bias, running_mean, running_var,
-                                                       momentum, eps, relu, save_mean, save_invstd, workspace, s);
+                                                       nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s);
     if (dtype == MBS_F32)
         return V == 4 ? bn_forward_t<float, 4>(x, residual, y, rows, C, weight, bias, running_mean, running_var,
-                                               momentum, eps, relu, save_mean, save_invstd, workspace, s)
+                                               nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s)
                       : bn_forward_t<float, 1>(x, residual, y, rows, C, weight, bias, running_mean, running_var,
-                                               momentum, eps, relu, save_mean, save_invstd, workspace, s);
+                                               nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s);
     return invalid("mbs_bn_forward: dtype must be MBS_BF16 or MBS_F32");
 }
 
