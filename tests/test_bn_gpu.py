@@ -301,3 +301,30 @@ def test_fused_resnet_dual_handles_match_autograd_adds(cuda, arch, monkeypatch):
         assert torch.equal(a, c)
     for a, c in zip(outs[0][2], outs[1][2]):
         assert torch.equal(a, c)
+
+
+def test_k5_dy2_contract_errors(cuda):
+    """mbs_bn_backward's dy2 is only accepted on the fused residual + ReLU path (include/mbs.h);
+    anything else is a loud MBS error, never a silent drop of the second gradient."""
+    from paper_2110_12484_b200 import _native
+    x, res, dy, w, b = _data(cuda, (4, 64, 6, 6), torch.bfloat16, seed=41)
+    rows, C = 4 * 36, 64
+    mean = torch.zeros(C, device=cuda)
+    inv = torch.ones(C, device=cuda)
+    dx = torch.empty_like(x)
+    ws = K5._workspace(rows, C, _native.BF16, cuda)
+    st = torch.cuda.current_stream().cuda_stream
+    lib = _native.lib()
+    # relu without residual + dy2: rejected
+    rc = lib.mbs_bn_backward(x.data_ptr(), None, dy.data_ptr(), dy.data_ptr(), dx.data_ptr(), None, _native.BF16, rows,
+                             C, w.data_ptr(), b.data_ptr(), mean.data_ptr(), inv.data_ptr(), 1, None, None,
+                             ws.data_ptr(), st)
+    assert rc != 0
+    # misaligned dy2 on the residual path: rejected (scalar path cannot take it)
+    dres = torch.empty_like(x)
+    flat = torch.empty(x.numel() + 1, device=cuda, dtype=x.dtype)
+    rc = lib.mbs_bn_backward(x.data_ptr(), res.data_ptr(), dy.data_ptr(), flat[1:].data_ptr(), dx.data_ptr(),
+                             dres.data_ptr(), _native.BF16, rows, C, w.data_ptr(), b.data_ptr(), mean.data_ptr(),
+                             inv.data_ptr(), 1, None, None, ws.data_ptr(), st)
+    assert rc != 0
+    torch.cuda.synchronize()
