@@ -278,10 +278,11 @@ int mbs_bn_backward(const void* x, const void* residual, const void* dy, const v
 int mbs_maxpool_forward(const void* x, void* y, uint8_t* idx, int dtype, int64_t N, int64_t H, int64_t W, int64_t C,
                         int k, int s, int p, void* stash, int64_t stash_C, int64_t stash_c0, void* stream);
 /* addend (nullable): dx += addend[..., add_c0:add_c0+C] (channels-last, add_C channels), summed in
- * fp32 before dx's single rounding (the skip-connection gradient, fused). */
-int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype, int64_t N, int64_t H, int64_t W,
-                         int64_t C, int k, int s, int p, const void* addend, int64_t add_C, int64_t add_c0,
-                         void* stream);
+ * fp32 before dx's single rounding (the skip-connection gradient, fused).
+ * dy2 (nullable): a second gradient of y (y has two consumers), added to dy in fp32 per window. */
+int mbs_maxpool_backward(const void* dy, const void* dy2, const uint8_t* idx, void* dx, int dtype, int64_t N,
+                         int64_t H, int64_t W, int64_t C, int k, int s, int p, const void* addend, int64_t add_C,
+                         int64_t add_c0, void* stream);
 /* Channel-slice copy between channels-last tensors seen as [M, C_total] rows:
  * dst[m, dst_c0 + c] = src[m, src_c0 + c] (+ bias[c], fp32, nullable) for c < C (the U-Net skip join
  * and its backward). colsum (nullable): fp32 [colsum_rows][C] per-CTA column sums of the copied

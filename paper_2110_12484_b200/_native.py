@@ -84,7 +84,7 @@ _SIGS = {
                                 c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "mbs_maxpool_forward": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64, c_int,
                                     c_int, c_int, c_void_p, c_int64, c_int64, c_void_p]),
-    "mbs_maxpool_backward": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64,
+    "mbs_maxpool_backward": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64,
                                      c_int, c_int, c_int, c_void_p, c_int64, c_int64, c_void_p]),
     "mbs_copy_channels": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p,
                                   c_void_p, c_int64, c_int, c_void_p]),

@@ -279,9 +279,13 @@ def _resnet_forward(self, x):
     """torchvision ResNet._forward_impl with every block output but the last handed on as two autograd
     handles (next block's conv1 and its skip / downsample): the gradient sum of the two consumers
     happens in K5's backward reduce of the producing block (mbs_bn_backward dy2), not in an autograd add."""
-    x = self.maxpool(self.relu(self.bn1(self.conv1(x))))
+    x = self.relu(self.bn1(self.conv1(x)))
     blocks = [b for layer in (self.layer1, self.layer2, self.layer3, self.layer4) for b in layer]
-    xm = xr = x
+    from .pool import MicroMaxPool2d
+    if isinstance(self.maxpool, MicroMaxPool2d) and x.is_cuda:
+        xm, xr = self.maxpool(x, dual=True)    # K6 sums the first block's two input gradients
+    else:
+        xm = xr = self.maxpool(x)
     for i, blk in enumerate(blocks):
         dual = i + 1 < len(blocks) and isinstance(blk, (FusedBottleneck, FusedBasicBlock))
         if isinstance(blk, (FusedBottleneck, FusedBasicBlock)):

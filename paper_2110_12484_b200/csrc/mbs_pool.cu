@@ -231,11 +231,13 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restric
 // W2 = 1: non-overlapping windows tiling the input (the U-Net 2x2/s2 pools) — no window search.
 // W2 = 2: 3x3 windows, stride 2 (the ResNet stem): at most 2x2 candidate windows, unrolled and
 // predicated so their index/gradient loads are all in flight at once.
+// dy2 (nullable): a second gradient of y (the pooled activation has two consumers), added to dy in
+// fp32 per window before the gather sum — in fp32 exactly torch's (dy1 + dy2) then gather.
 template <typename T, int V, typename I, int W2>
 __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restrict__ dy,
                                                               const uint8_t* __restrict__ idx, T* __restrict__ dx,
                                                               PoolGeomT<I> g, const T* __restrict__ add, I aC,
-                                                              I ac0) {
+                                                              I ac0, const T* __restrict__ dy2) {
     cudaGridDependencySynchronize();
     const I cv = g.C / V;
     const I total = g.N * g.H * g.W * cv;
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
             // all four candidate windows' idx / dy loaded first (out-of-range ones from a valid
             // address, skipped below), then summed in ascending (oh, ow) order
             using IRaw = typename std::conditional<V == 8, uint2, uint32_t>::type;
-            uint4 draw[4];
+            uint4 draw[4], draw2[4];
             IRaw iraw[4];
             bool ok[4];
             uint8_t pos[4];
@@ -276,6 +278,7 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
                 const I o = ok[q2] ? ((n * g.Ho + oh) * g.Wo + ow) * g.C + c0 : (I)0;
                 iraw[q2] = __ldg(reinterpret_cast<const IRaw*>(idx + o));
                 draw[q2] = __ldg(reinterpret_cast<const uint4*>(dy + o));
+                if (dy2) draw2[q2] = __ldg(reinterpret_cast<const uint4*>(dy2 + o));
             }
 #pragma unroll
             for (int q2 = 0; q2 < 4; ++q2) {
@@ -284,6 +287,12 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
                 float d[V];
                 load_idx<V>(reinterpret_cast<const uint8_t*>(&iraw[q2]), a);
                 PoolIO<T, V>::load(reinterpret_cast<const T*>(&draw[q2]), d);
+                if (dy2) {
+                    float d2[V];
+                    PoolIO<T, V>::load(reinterpret_cast<const T*>(&draw2[q2]), d2);
+#pragma unroll
+                    for (int i = 0; i < V; ++i) d[i] += d2[i];
+                }
 #pragma unroll
                 for (int i = 0; i < V; ++i)
                     if (a[i] == pos[q2]) acc[i] += d[i];
@@ -297,6 +306,12 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
             float d[V];
             load_idx<V>(idx + o, a);
             PoolIO<T, V>::load(dy + o, d);
+            if (dy2) {
+                float d2[V];
+                PoolIO<T, V>::load(dy2 + o, d2);
+#pragma unroll
+                for (int i = 0; i < V; ++i) d[i] += d2[i];
+            }
 #pragma unroll
             for (int i = 0; i < V; ++i)
                 if (a[i] == pos) acc[i] = d[i];
@@ -313,6 +328,12 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
                     float d[V];
                     load_idx<V>(idx + o, a);
                     PoolIO<T, V>::load(dy + o, d);
+                    if (dy2) {
+                        float d2[V];
+                        PoolIO<T, V>::load(dy2 + o, d2);
+#pragma unroll
+                        for (int i = 0; i < V; ++i) d[i] += d2[i];
+                    }
 #pragma unroll
                     for (int i = 0; i < V; ++i)
                         if (a[i] == pos) acc[i] += d[i];
@@ -456,8 +477,8 @@ static int maxpool_fwd(const void* x, void* y, uint8_t* idx, int dtype, const Po
 }
 
 template <typename I, int W2>
-static int maxpool_bwd(const void* dy, const uint8_t* idx, void* dx, int dtype, const PoolGeom& g0, const void* add,
-                       int64_t aC, int64_t ac0, cudaStream_t cs) {
+static int maxpool_bwd(const void* dy, const void* dy2, const uint8_t* idx, void* dx, int dtype, const PoolGeom& g0,
+                       const void* add, int64_t aC, int64_t ac0, cudaStream_t cs) {
     const PoolGeomT<I> gv = narrow<I>(g0, dtype == MBS_BF16 ? 8 : 4), g1 = narrow<I>(g0, 1);
     const int64_t ins = g0.N * g0.H * g0.W;
     const int es = dtype == MBS_BF16 ? 2 : 4;
@@ -467,19 +488,19 @@ static int maxpool_bwd(const void* dy, const uint8_t* idx, void* dx, int dtype, 
     cudaError_t e;
     if (dtype == MBS_BF16) {
         using T = __nv_bfloat16;
-        if (g0.C % 8 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7) && add_vec)
+        if (g0.C % 8 == 0 && aligned16(dy, dx, dy2) && !(reinterpret_cast<uintptr_t>(idx) & 7) && add_vec)
             e = pool_launch(k_maxpool_bwd<T, 8, I, W2>, ins * (g0.C / 8), cs, (const T*)dy, idx, (T*)dx, gv, (const T*)add,
-                            iaC, iac0);
+                            iaC, iac0, (const T*)dy2);
         else
             e = pool_launch(k_maxpool_bwd<T, 1, I, W2>, ins * g0.C, cs, (const T*)dy, idx, (T*)dx, g1, (const T*)add, iaC,
-                            iac0);
+                            iac0, (const T*)dy2);
     } else {
-        if (g0.C % 4 == 0 && aligned16(dy, dx, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 3) && add_vec)
+        if (g0.C % 4 == 0 && aligned16(dy, dx, dy2) && !(reinterpret_cast<uintptr_t>(idx) & 3) && add_vec)
             e = pool_launch(k_maxpool_bwd<float, 4, I, W2>, ins * (g0.C / 4), cs, (const float*)dy, idx, (float*)dx, gv,
-                            (const float*)add, iaC, iac0);
+                            (const float*)add, iaC, iac0, (const float*)dy2);
         else
             e = pool_launch(k_maxpool_bwd<float, 1, I, W2>, ins * g0.C, cs, (const float*)dy, idx, (float*)dx, g1,
-                            (const float*)add, iaC, iac0);
+                            (const float*)add, iaC, iac0, (const float*)dy2);
     }
     MBS_CK(e);
     return MBS_OK;
@@ -531,9 +552,9 @@ int mbs_maxpool_forward(const void* x, void* y, uint8_t* idx, int dtype, int64_t
                : maxpool_fwd<int64_t>(x, y, idx, dtype, g, stash, stash_C, stash_c0, cs);
 }
 
-int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype, int64_t N, int64_t H, int64_t W,
-                         int64_t C, int k, int s, int p, const void* addend, int64_t add_C, int64_t add_c0,
-                         void* stream) {
+int mbs_maxpool_backward(const void* dy, const void* dy2, const uint8_t* idx, void* dx, int dtype, int64_t N,
+                         int64_t H, int64_t W, int64_t C, int k, int s, int p, const void* addend, int64_t add_C,
+                         int64_t add_c0, void* stream) {
     if (!dy || !idx || !dx) return invalid("mbs_maxpool_backward: null pointer");
     PoolGeom g;
     int st = pool_check(dtype, N, H, W, C, k, s, p, &g);
@@ -543,14 +564,14 @@ int mbs_maxpool_backward(const void* dy, const uint8_t* idx, void* dx, int dtype
     const bool i32 = fits_i32(g.N * g.H * g.W * std::max<int64_t>(g.C, addend ? add_C : 0)) &&
                      fits_i32(g.N * g.Ho * g.Wo * g.C);
     const bool w2 = g.k == g.s && g.p == 0 && g.H % g.k == 0 && g.W % g.k == 0;   // one window per element
-    const bool k3s2 = g.k == 3 && g.s == 2 && g.C % (dtype == MBS_BF16 ? 8 : 4) == 0 && aligned16(dy, dx, nullptr) &&
+    const bool k3s2 = g.k == 3 && g.s == 2 && g.C % (dtype == MBS_BF16 ? 8 : 4) == 0 && aligned16(dy, dx, dy2) &&
                       !(reinterpret_cast<uintptr_t>(idx) & (dtype == MBS_BF16 ? 7 : 3));
     if (i32)
-        return w2     ? maxpool_bwd<int32_t, 1>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs)
-               : k3s2 ? maxpool_bwd<int32_t, 2>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs)
-                      : maxpool_bwd<int32_t, 0>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs);
-    return w2 ? maxpool_bwd<int64_t, 1>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs)
-              : maxpool_bwd<int64_t, 0>(dy, idx, dx, dtype, g, addend, add_C, add_c0, cs);
+        return w2     ? maxpool_bwd<int32_t, 1>(dy, dy2, idx, dx, dtype, g, addend, add_C, add_c0, cs)
+               : k3s2 ? maxpool_bwd<int32_t, 2>(dy, dy2, idx, dx, dtype, g, addend, add_C, add_c0, cs)
+                      : maxpool_bwd<int32_t, 0>(dy, dy2, idx, dx, dtype, g, addend, add_C, add_c0, cs);
+    return w2 ? maxpool_bwd<int64_t, 1>(dy, dy2, idx, dx, dtype, g, addend, add_C, add_c0, cs)
+              : maxpool_bwd<int64_t, 0>(dy, dy2, idx, dx, dtype, g, addend, add_C, add_c0, cs);
 }
 
 int mbs_copy_channels(const void* src, int64_t src_C, int64_t src_c0, void* dst, int64_t dst_C, int64_t dst_c0,

@@ -32,7 +32,7 @@ def _square(v):
 
 class _MaxPoolFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, k, s, p):
+    def forward(ctx, x, k, s, p, dual=False):
         code = _DTYPES.get(x.dtype)
         if code is None:
             raise ValueError(f"K6 max-pool supports bfloat16 / float32, got {x.dtype}")
@@ -47,22 +47,29 @@ class _MaxPoolFn(torch.autograd.Function):
                                                         k, s, p, None, 0, 0, stream.cuda_stream), "mbs_maxpool_forward")
         ctx.save_for_backward(idx)
         ctx.geom = (n, c, h, w, k, s, p, code)
+        if dual:   # two autograd handles: the consumers' gradients are summed inside the backward gather
+            ctx.set_materialize_grads(False)
+            return y, y.view_as(y)
         return y
 
     @staticmethod
-    def backward(ctx, dy):
+    def backward(ctx, dy, dy2=None):
         (idx,) = ctx.saved_tensors
         n, c, h, w, k, s, p, code = ctx.geom
-        dy = dy.contiguous(memory_format=torch.channels_last)
-        if _DTYPES.get(dy.dtype) != code:
-            dy = dy.to(idx.device).to({_native.BF16: torch.bfloat16, _native.F32: torch.float32}[code])
+        if dy is None:
+            dy, dy2 = dy2, None
+        dt = {_native.BF16: torch.bfloat16, _native.F32: torch.float32}[code]
+        dy = dy.to(dt).contiguous(memory_format=torch.channels_last)
+        if dy2 is not None:
+            dy2 = dy2.to(dt).contiguous(memory_format=torch.channels_last)
         dx = torch.empty((n, c, h, w), dtype=dy.dtype, device=dy.device, memory_format=torch.channels_last)
         stream = torch.cuda.current_stream(dy.device)
         TIMER.launches += 1
-        _native.check(_native.lib().mbs_maxpool_backward(dy.data_ptr(), idx.data_ptr(), dx.data_ptr(), code, n, h, w,
+        _native.check(_native.lib().mbs_maxpool_backward(dy.data_ptr(), None if dy2 is None else dy2.data_ptr(),
+                                                         idx.data_ptr(), dx.data_ptr(), code, n, h, w,
                                                          c, k, s, p, None, 0, 0, stream.cuda_stream),
                       "mbs_maxpool_backward")
-        return dx, None, None, None
+        return dx, None, None, None, None
 
 
 class _PoolStashFn(torch.autograd.Function):
@@ -104,7 +111,7 @@ class _PoolStashFn(torch.autograd.Function):
         stream = torch.cuda.current_stream(dy.device)
         TIMER.launches += 1
         _native.check(_native.lib().mbs_maxpool_backward(
-            dy.data_ptr(), idx.data_ptr(), dx.data_ptr(), code, n, h, w, c, k, k, 0,
+            dy.data_ptr(), None, idx.data_ptr(), dx.data_ptr(), code, n, h, w, c, k, k, 0,
             None if dbuf is None else dbuf.data_ptr(), ctot, 0, stream.cuda_stream), "mbs_maxpool_backward(addend)")
         return dx, None, None
 
@@ -169,18 +176,20 @@ def join_skip(buf, up, bias=None):
     return _JoinFn.apply(buf, up, bias, buf.shape[1] - up.shape[1])
 
 
-def max_pool2d(x, kernel_size: int, stride: int | None = None, padding: int = 0):
-    """Functional K6 max-pool (square window, dilation 1, floor mode)."""
-    return _MaxPoolFn.apply(x, int(kernel_size), int(stride or kernel_size), int(padding))
+def max_pool2d(x, kernel_size: int, stride: int | None = None, padding: int = 0, dual: bool = False):
+    """Functional K6 max-pool (square window, dilation 1, floor mode); ``dual``: the output as two
+    autograd handles whose gradients are summed inside the backward kernel."""
+    return _MaxPoolFn.apply(x, int(kernel_size), int(stride or kernel_size), int(padding), dual)
 
 
 class MicroMaxPool2d(nn.MaxPool2d):
     """``nn.MaxPool2d`` whose CUDA forward/backward run K6 (bit-identical to torch)."""
 
-    def forward(self, x):
+    def forward(self, x, dual: bool = False):
         if not x.is_cuda or x.dim() != 4:
-            return super().forward(x)
-        return _MaxPoolFn.apply(x, self._k, self._s, self._p)
+            y = super().forward(x)
+            return (y, y) if dual else y
+        return _MaxPoolFn.apply(x, self._k, self._s, self._p, dual)
 
 
 def supported(m: nn.MaxPool2d) -> bool:

@@ -284,10 +284,11 @@ def test_fused_resnet_dual_handles_match_autograd_adds(cuda, arch, monkeypatch):
     monkeypatch.setattr(torch.backends.cudnn, "benchmark", False)
     torch.manual_seed(0)
     net = getattr(torchvision.models, arch)(num_classes=10).to(cuda).to(memory_format=torch.channels_last).train()
+    from paper_2110_12484_b200 import pool as K6
     monkeypatch.setenv("MBS_K5_DUAL", "1")
-    dual = K5.fuse_batchnorm(copy.deepcopy(net))
+    dual = K6.swap_maxpool(K5.fuse_batchnorm(copy.deepcopy(net)))     # K6 stem pool: dual output too
     monkeypatch.setenv("MBS_K5_DUAL", "0")
-    plain = K5.fuse_batchnorm(copy.deepcopy(net))
+    plain = K6.swap_maxpool(K5.fuse_batchnorm(copy.deepcopy(net)))
     assert type(dual) is K5.FusedResNet and type(plain) is not K5.FusedResNet
     assert list(dual.state_dict()) == list(net.state_dict())
     x = torch.randn(6, 3, 64, 64, device=cuda).contiguous(memory_format=torch.channels_last)

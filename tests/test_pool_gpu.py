@@ -123,3 +123,26 @@ def test_unet_native_skips_match_plain(cuda):
     assert torch.allclose(outs[0][0], outs[1][0], rtol=1e-5, atol=1e-6)
     for ga, gb in zip(outs[0][1], outs[1][1]):
         assert torch.allclose(ga, gb, rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("case", [((4, 64, 112, 112), 3, 2, 1), ((2, 24, 17, 13), 3, 2, 1), ((3, 64, 48, 48), 2, 2, 0),
+                                  ((2, 8, 9, 9), 3, 1, 1), ((2, 5, 11, 7), 2, 2, 0)])
+def test_k6_dual_output_fp32_bit_identical_to_summed_gradient(cuda, case):
+    """Dual output (the pooled activation feeds two consumers): K6 adds the two gradients in fp32 per
+    window before the gather — in fp32 exactly torch's (dy1 + dy2) then gather, so dx is bit-identical;
+    one unused handle (gradient None) is the single-output backward."""
+    shape, k, s, p = case
+    x = torch.randn(shape, device=cuda).contiguous(memory_format=torch.channels_last)
+    xa = x.clone().requires_grad_(True)
+    y1, y2 = K6.max_pool2d(xa, k, s, p, dual=True)
+    g1, g2 = torch.randn_like(y1), torch.randn_like(y1)
+    torch.autograd.backward([y1, y2], [g1, g2])
+    xb = x.clone().requires_grad_(True)
+    F.max_pool2d(xb, k, s, p).backward(g1 + g2)
+    assert torch.equal(xa.grad, xb.grad)
+    xc = x.clone().requires_grad_(True)
+    _, y2 = K6.max_pool2d(xc, k, s, p, dual=True)
+    y2.backward(g2)
+    xd = x.clone().requires_grad_(True)
+    F.max_pool2d(xd, k, s, p).backward(g2)
+    assert torch.equal(xc.grad, xd.grad)
