@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <type_traits>
@@ -348,6 +349,81 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
     }
 }
 
+// 3x3 / stride 2 / pad 1 (the ResNet stem) backward on 2x2 input blocks: input rows 2a, 2a+1 and
+// columns 2b, 2b+1 lie in windows oh in {a, a+1}, ow in {b, b+1} only, so one thread loads those 4
+// windows' idx/dy once (all in flight) and serves 4 input pixels with the 9 (pixel, window) pairs
+// that exist — the per-pixel kernel evaluated 16 candidate slots for every 4 pixels.
+// Each pixel sums its windows in ascending (oh, ow) order in fp32: bit-identical to torch.
+template <typename T, int V>
+__global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd_blk(const T* __restrict__ dy,
+                                                                  const uint8_t* __restrict__ idx,
+                                                                  T* __restrict__ dx, PoolGeomT<int32_t> g,
+                                                                  const T* __restrict__ dy2) {
+    static_assert(sizeof(T) * V == 16, "16-byte channel vectors");
+    using IRaw = typename std::conditional<V == 8, uint2, uint32_t>::type;
+    cudaGridDependencySynchronize();
+    const int cv = g.C / V;
+    const int total = g.N * g.Ho * g.Wo * cv;   // blocks: Hb = Ho, Wb = Wo for k3/s2/p1
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        int q = g.cv.div(t);
+        const int c0 = (t - q * cv) * V;
+        int q2 = g.dWo.div(q);
+        const int b = q - q2 * g.Wo;
+        const int n = g.dHo.div(q2);
+        const int a = q2 - n * g.Ho;
+        uint4 dr[4], dr2[4];
+        IRaw ir[4];
+        bool ok[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int oh = a + w / 2, ow = b + w % 2;
+            ok[w] = oh < g.Ho && ow < g.Wo;
+            const int o = ok[w] ? ((n * g.Ho + oh) * g.Wo + ow) * g.C + c0 : 0;
+            ir[w] = __ldg(reinterpret_cast<const IRaw*>(idx + o));
+            dr[w] = __ldg(reinterpret_cast<const uint4*>(dy + o));
+            if (dy2) dr2[w] = __ldg(reinterpret_cast<const uint4*>(dy2 + o));
+        }
+        float d[4][V];
+        uint8_t ai[4][V];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            PoolIO<T, V>::load(reinterpret_cast<const T*>(&dr[w]), d[w]);
+            load_idx<V>(reinterpret_cast<const uint8_t*>(&ir[w]), ai[w]);
+            if (dy2) {
+                float d2[V];
+                PoolIO<T, V>::load(reinterpret_cast<const T*>(&dr2[w]), d2);
+#pragma unroll
+                for (int i = 0; i < V; ++i) d[w][i] += d2[i];
+            }
+        }
+#pragma unroll
+        for (int dh = 0; dh < 2; ++dh) {
+#pragma unroll
+            for (int dw = 0; dw < 2; ++dw) {
+                const int ih = 2 * a + dh, iw = 2 * b + dw;
+                if (ih >= g.H || iw >= g.W) continue;
+                float acc[V];
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[i] = 0.f;
+#pragma unroll
+                for (int wh = 0; wh < 2; ++wh) {
+#pragma unroll
+                    for (int ww = 0; ww < 2; ++ww) {
+                        if ((wh == 1 && dh == 0) || (ww == 1 && dw == 0)) continue;   // not in that window
+                        const int w = wh * 2 + ww;
+                        const uint8_t pos = (uint8_t)((dh + 1 - 2 * wh) * 3 + (dw + 1 - 2 * ww));
+                        if (!ok[w]) continue;
+#pragma unroll
+                        for (int i = 0; i < V; ++i)
+                            if (ai[w][i] == pos) acc[i] += d[w][i];
+                    }
+                }
+                PoolIO<T, V>::store(dx + ((n * g.H + ih) * g.W + iw) * g.C + c0, acc);
+            }
+        }
+    }
+}
+
 // Channel-slice copy between channels-last tensors viewed as [M, C_total] rows:
 // dst[m, dc0 + c] = src[m, sc0 + c] (+ bias[c]) — the U-Net skip join (the upsampled half lands in
 // the concat buffer with its ConvTranspose bias added on the way) and its backward (the slice made
@@ -440,6 +516,11 @@ static int pool_check(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
 
 static bool aligned16(const void* a, const void* b, const void* c) {
     return !((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(c)) & 15);
+}
+
+static bool block_mode() {   // A/B: MBS_K6_BLOCK=0 keeps the per-pixel 3x3/s2 backward
+    const char* e = getenv("MBS_K6_BLOCK");
+    return !e || atoi(e) != 0;
 }
 
 static bool fits_i32(int64_t v) { return v < (int64_t)INT32_MAX - (1 << 22); }  // grid-stride headroom
@@ -566,6 +647,18 @@ int mbs_maxpool_backward(const void* dy, const void* dy2, const uint8_t* idx, vo
     const bool w2 = g.k == g.s && g.p == 0 && g.H % g.k == 0 && g.W % g.k == 0;   // one window per element
     const bool k3s2 = g.k == 3 && g.s == 2 && g.C % (dtype == MBS_BF16 ? 8 : 4) == 0 && aligned16(dy, dx, dy2) &&
                       !(reinterpret_cast<uintptr_t>(idx) & (dtype == MBS_BF16 ? 7 : 3));
+    if (k3s2 && g.p == 1 && i32 && !addend && block_mode()) {
+        const int V = dtype == MBS_BF16 ? 8 : 4;
+        const PoolGeomT<int32_t> gv = narrow<int32_t>(g, V);
+        const int64_t work = g.N * g.Ho * g.Wo * (g.C / V);
+        cudaError_t e = dtype == MBS_BF16
+            ? pool_launch(k_maxpool_bwd_blk<__nv_bfloat16, 8>, work, cs, (const __nv_bfloat16*)dy, idx,
+                          (__nv_bfloat16*)dx, gv, (const __nv_bfloat16*)dy2)
+            : pool_launch(k_maxpool_bwd_blk<float, 4>, work, cs, (const float*)dy, idx, (float*)dx, gv,
+                          (const float*)dy2);
+        MBS_CK(e);
+        return MBS_OK;
+    }
     if (i32)
         return w2     ? maxpool_bwd<int32_t, 1>(dy, dy2, idx, dx, dtype, g, addend, add_C, add_c0, cs)
                : k3s2 ? maxpool_bwd<int32_t, 2>(dy, dy2, idx, dx, dtype, g, addend, add_C, add_c0, cs)
