@@ -145,8 +145,8 @@ __device__ __forceinline__ void load_idx(const uint8_t* p, uint8_t (&v)[V]) {
 // k | H, k | W) every input element is read exactly once, so the kernel also writes it into channel
 // columns [sc0, sc0 + C) of a wider channels-last tensor with row stride sC — the U-Net skip
 // connection lands in its concat buffer without a separate torch.cat pass.
-// K > 0: the window size is a compile-time constant (the ResNet stem's 3x3): the window loops unroll
-// and all k*k loads are in flight at once instead of one per loop trip (no stash on this variant).
+// K > 0: the window size is a compile-time constant (the ResNet stem's 3x3, the U-Net's 2x2): the
+// window loops unroll and all k*k loads are in flight at once instead of one per loop trip.
 template <typename T, int V, typename I, int K = 0>
 __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restrict__ x, T* __restrict__ y,
                                                               uint8_t* __restrict__ idx, PoolGeomT<I> g,
@@ -185,6 +185,14 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restric
                 ok[q2] = ih >= 0 && ih < g.H && iw >= 0 && iw < g.W;
                 const I pix = ok[q2] ? (n * g.H + ih) * g.W + iw : (I)0;
                 raw[q2] = __ldg(reinterpret_cast<const uint4*>(x + pix * g.C + c0));
+            }
+            if (stash) {   // after every load is issued
+#pragma unroll
+                for (int q2 = 0; q2 < K * K; ++q2) {
+                    const I ih = h0 + q2 / K, iw = w0 + q2 % K;
+                    if (ok[q2])
+                        *reinterpret_cast<uint4*>(stash + ((n * g.H + ih) * g.W + iw) * sC + sc0 + c0) = raw[q2];
+                }
             }
             if constexpr (sizeof(T) == 2) {
                 // bf16: the scan on packed bf16x2 lanes — lane masks from the same ordered ">" and NaN
@@ -566,11 +574,12 @@ static int maxpool_fwd(const void* x, void* y, uint8_t* idx, int dtype, const Po
     if (dtype == MBS_BF16) {
         using T = __nv_bfloat16;
         if (g0.C % 8 == 0 && aligned16(x, y, nullptr) && !(reinterpret_cast<uintptr_t>(idx) & 7) && stash_vec)
-            e = (g0.k == 3 && !stash)
-                    ? pool_launch(k_maxpool_fwd<T, 8, I, 3>, outs * (g0.C / 8), cs, (const T*)x, (T*)y, idx, gv,
-                                  (T*)nullptr, isC, isc0)
-                    : pool_launch(k_maxpool_fwd<T, 8, I>, outs * (g0.C / 8), cs, (const T*)x, (T*)y, idx, gv,
-                                  (T*)stash, isC, isc0);
+            e = g0.k == 3 ? pool_launch(k_maxpool_fwd<T, 8, I, 3>, outs * (g0.C / 8), cs, (const T*)x, (T*)y, idx, gv,
+                                        (T*)stash, isC, isc0)
+              : g0.k == 2 ? pool_launch(k_maxpool_fwd<T, 8, I, 2>, outs * (g0.C / 8), cs, (const T*)x, (T*)y, idx, gv,
+                                        (T*)stash, isC, isc0)
+                          : pool_launch(k_maxpool_fwd<T, 8, I>, outs * (g0.C / 8), cs, (const T*)x, (T*)y, idx, gv,
+                                        (T*)stash, isC, isc0);
         else
             e = pool_launch(k_maxpool_fwd<T, 1, I>, outs * g0.C, cs, (const T*)x, (T*)y, idx, g1, (T*)stash, isC, isc0);
     } else {
