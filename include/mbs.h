@@ -199,6 +199,11 @@ int mbs_streamer_release(mbs_streamer_t h, int slot, void* compute_stream);
  * job's events; records are kept for the last 256 jobs. */
 int mbs_streamer_timing(mbs_streamer_t h, int64_t job, double* gather_ms, double* copy_ms,
                         double* blocked_ms, int64_t* bytes);
+/* Absolute copy times of a job: copy start / end in ms after `origin_event` (a cudaEvent_t recorded with
+ * timing, e.g. torch.cuda.Event(enable_timing=True).cuda_event) — the "transfer" StreamEvent of the
+ * reference's schedule (streaming.py:41-46) measured on the copy stream. Blocks until the copy ended. */
+int mbs_streamer_timeline(mbs_streamer_t h, int64_t job, void* origin_event, double* copy_start_ms,
+                          double* copy_end_ms);
 /* Multi-threaded host gather into a caller buffer (used by tests and the
  * epoch driver): dst[r] = src[rows[r]] for row_bytes-sized rows. */
 int mbs_host_gather(const void* src, int64_t row_bytes, const int64_t* rows, int64_t n_rows,

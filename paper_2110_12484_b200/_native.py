@@ -67,6 +67,7 @@ _SIGS = {
     "mbs_streamer_release": (c_int, [c_void_p, c_int, c_void_p]),
     "mbs_streamer_timing": (c_int, [c_void_p, c_int64, POINTER(c_double), POINTER(c_double), POINTER(c_double),
                                     POINTER(c_int64)]),
+    "mbs_streamer_timeline": (c_int, [c_void_p, c_int64, c_void_p, POINTER(c_double), POINTER(c_double)]),
     "mbs_host_gather": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int]),
     "mbs_peer_create": (c_int, [c_int, c_int, c_int64, POINTER(c_void_p)]),
     "mbs_peer_handle": (c_int, [c_void_p, c_void_p]),

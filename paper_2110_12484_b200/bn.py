@@ -105,8 +105,9 @@ class _MicroBatchNormFn(torch.autograd.Function):
             if residual.shape != x.shape:
                 raise ValueError(f"residual shape {tuple(residual.shape)} != {tuple(x.shape)}")
         rows, C = _geometry(x)
-        if rows < 2:
-            raise ValueError(f"Expected more than 1 value per channel when training, got input size {list(x.shape)}")
+        # rows == 1 (one value per channel, e.g. a 1-sample tail micro-batch on a 1x1 map) is legal, as in the
+        # reference (eps-guarded): x_hat = 0, y = beta, dx = 0, and the running variance takes the
+        # biased (= reference, nn.py:329-332) variance 0. torch's BatchNorm raises here instead.
         y = torch.empty_like(x)
         mean = torch.empty(C, dtype=torch.float32, device=x.device)
         invstd = torch.empty_like(mean)

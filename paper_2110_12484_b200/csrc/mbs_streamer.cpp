@@ -400,6 +400,26 @@ int mbs_streamer_timing(mbs_streamer_t h, int64_t job, double* gather_ms, double
     return MBS_OK;
 }
 
+int mbs_streamer_timeline(mbs_streamer_t h, int64_t job, void* origin_event, double* copy_start_ms,
+                          double* copy_end_ms) {
+    if (!h || job < 0 || !origin_event) return invalid("mbs_streamer_timeline: bad arguments");
+    {
+        std::unique_lock<std::mutex> lk(h->m);
+        if (job >= h->next_seq || job < h->next_seq - (int64_t)h->ring.size())
+            return invalid("mbs_streamer_timeline: job record no longer (or not yet) available");
+        h->cv.wait(lk, [&] { return job < h->issued_count; });
+    }
+    JobRec& r = h->rec(job);
+    auto origin = (cudaEvent_t)origin_event;
+    MBS_CK(cudaEventSynchronize(r.ready));
+    float a = 0.f, b = 0.f;
+    MBS_CK(cudaEventElapsedTime(&a, origin, r.start));
+    MBS_CK(cudaEventElapsedTime(&b, origin, r.ready));
+    if (copy_start_ms) *copy_start_ms = a;
+    if (copy_end_ms) *copy_end_ms = b;
+    return MBS_OK;
+}
+
 int mbs_host_gather(const void* src, int64_t row_bytes, const int64_t* rows, int64_t n_rows, void* dst,
                     int n_threads) {
     if (!src || !dst || !rows || row_bytes < 1 || n_rows < 0) return invalid("mbs_host_gather: bad arguments");

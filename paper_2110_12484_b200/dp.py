@@ -35,7 +35,7 @@ import numpy as np
 import torch
 
 from .engine import (GradientAccumulator, MicroBatchPlan, MiniBatchStats, _as_tensor, _micro_source, make_streamer,
-                     normalization_factor, plan_split, weight_cast_cache, _graph_for)
+                     normalization_factor, plan_split, weight_cast_cache, _graph_dest, _graph_for)
 from .losses import compute_loss
 from .optim import apply_update
 from .tensor import ParameterSet
@@ -203,9 +203,9 @@ class _Result:
             h = self._host.tolist()
             n = self._n
             self._r = dict(loss=h[0], losses_raw=h[1:1 + n], losses_normalized=h[1 + n:1 + 2 * n], norm2=h[-1])
-            if not math.isfinite(h[-1]):
+            if not (math.isfinite(h[-1]) and all(math.isfinite(v) for v in h[:-1])):
                 from .errors import NonFiniteError
-                raise NonFiniteError(-1, "non-finite accumulated gradient; the optimizer step was skipped")
+                raise NonFiniteError(-1, "non-finite accumulated gradient or micro-batch loss; no update was applied")
         return self._r
 
     loss = property(lambda s: s.resolve()["loss"])
@@ -307,7 +307,9 @@ class DataParallelMBS:
         if x.device.type == "cpu" and streamer is None:
             streamer = own = make_streamer(x, y, n_mu)
         try:
-            source = iter(_micro_source(x, y, jobs, staging, prefetch, streamer))
+            dest = _graph_dest(model, accumulator, loss_kind, autocast_dtype, loss_from_logits, dice_smoothing,
+                               "fused")
+            source = iter(_micro_source(x, y, jobs, staging, prefetch, streamer, dest))
             return self._step(model, plan, block, source, normalization, loss_kind, optimizer_state, accumulator,
                               autocast_dtype, loss_from_logits, dice_smoothing, lr_for_step)
         finally:
@@ -357,12 +359,12 @@ class DataParallelMBS:
             streamer = own = make_streamer(x, y, micro_batch_size)
         out = []
         try:
-            source = iter(_micro_source(x, y, jobs, staging, prefetch, streamer))
+            dest = _graph_dest(model, accumulator, loss_kind, autocast_dtype, loss_from_logits, dice_smoothing,
+                               "fused")
+            source = iter(_micro_source(x, y, jobs, staging, prefetch, streamer, dest))
             for _ in range(0, n, mini_batch_size):
                 r = self._step(model, plan, block, source, normalization, loss_kind, optimizer_state, accumulator,
                                autocast_dtype, loss_from_logits, dice_smoothing, lr_for_step)
-                if out:
-                    out[-1].resolve()          # one mini-batch behind: no stall
                 out.append(r)
             for r in out:
                 r.resolve()
@@ -497,9 +499,10 @@ class DataParallelMBS:
         if bn is not None:
             bn.merge(block, plan.n_s_mu)
         total = acc.as_gradient_set()
+        res = _Result(rec, stats_dev[0], plan.n_s_mu)
+        res.resolve()        # NonFiniteError before the update on every rank (reference: nn.py:578-579)
         if lr_for_step is not None:
             optimizer_state.lr = lr_for_step(optimizer_state.step_count)
         apply_update(self.params, total, optimizer_state)
-        res = _Result(rec, stats_dev[0], plan.n_s_mu)
         res.step_count = optimizer_state.step_count
         return res

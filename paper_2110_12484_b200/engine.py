@@ -29,8 +29,9 @@ accumulated gradients agree to fp32 rounding (tests/test_engine_gpu.py).
 from __future__ import annotations
 
 import ctypes
-import os
 import math
+import os
+import weakref
 from contextlib import nullcontext
 from dataclasses import dataclass, field
 from typing import Callable
@@ -289,6 +290,8 @@ class GradientAccumulator:
         """K1 over every segment from a prebuilt device-pointer table (a captured micro step's gradients)."""
         lp = None
         if loss is not None:
+            if loss.dtype != torch.float32:      # K1 reads the loss slot as fp32
+                loss = loss.detach().float()
             lp = loss.data_ptr()
         lf = float(factor if loss_factor is None else loss_factor)
         t0 = TIMER.start(stream)
@@ -407,8 +410,11 @@ class MiniBatchStats:
     """Per-mini-batch observables (engine.py:166-176), copied off the device asynchronously.
 
     Reading any field synchronises on that copy; a non-finite accumulated
-    gradient raises ``NonFiniteError`` there (the optimizer step was already
-    suppressed on device, so the parameters are intact).
+    gradient or micro-batch loss raises ``NonFiniteError`` there.
+    ``train_mini_batch`` / ``train_epoch`` resolve it before the optimizer
+    step, so on a non-finite mini-batch the parameters, the optimizer moments
+    and ``step_count`` are exactly where the reference leaves them (it raises
+    in the forward, ``nn.py:578-579``, before any update).
     """
 
     def __init__(self, stats_dev: torch.Tensor, n_micro: int, max_micro: int, outputs: list, stream=None):
@@ -486,12 +492,27 @@ def _as_tensor(a):
     return torch.from_numpy(np.ascontiguousarray(a))
 
 
-def _micro_source(x, y, jobs, staging, prefetch, streamer):
+def _micro_source(x, y, jobs, staging, prefetch, streamer, dest=None, tracer=None):
     if x.device.type == "cuda":
-        return device_micro_batches(x, y.to(x.device) if y.device != x.device else y, jobs, staging)
+        return device_micro_batches(x, y.to(x.device) if y.device != x.device else y, jobs, staging, dest=dest,
+                                    tracer=tracer)
     if streamer is None:
         raise ValueError("host-resident inputs need a MicroBatchStreamer (pass streamer=...)")
-    return streamer.stream(x, y, jobs, staging, prefetch=prefetch)
+    return streamer.stream(x, y, jobs, staging, prefetch=prefetch, dest=dest, tracer=tracer)
+
+
+def _graph_dest(model, acc, loss_kind, autocast_dtype, loss_from_logits, dice_smoothing, normalize_via):
+    """Where the sources stage a micro-batch: the static buffers of its captured micro step when one exists
+    (K2 then writes the model input once), else a fresh tensor (None)."""
+    if not (CUDA_GRAPHS and normalize_via == "fused" and model.training):
+        return None
+    from . import graphs
+    plist = acc._plist
+
+    def dest(x_shape, x_dtype, channels_last, y_shape, y_dtype):
+        return graphs.static_buffers(model, plist, loss_kind, x_shape, x_dtype, channels_last, y_shape, y_dtype,
+                                     autocast_dtype, loss_from_logits, dice_smoothing)
+    return dest
 
 
 def make_streamer(x: torch.Tensor, y: torch.Tensor, max_rows: int, *, n_slots: int = 3, n_threads=None):
@@ -507,12 +528,13 @@ def mini_batch_gradient(model: torch.nn.Module, params: ParameterSet, x, y, plan
                         accumulator: GradientAccumulator | None = None, normalize_via: str = "fused",
                         forward_mode: str = "train", staging: Staging | None = None,
                         autocast_dtype: torch.dtype | None = None, streamer: MicroBatchStreamer | None = None,
-                        keep_outputs: bool = True) -> tuple:
+                        keep_outputs: bool = True, tracer=None, _close_trace: bool = True) -> tuple:
     """Accumulated gradient of one mini-batch, micro-batch by micro-batch (engine.py:179-230).
 
     ``x``/``y`` are device tensors (sliced / staged in HBM) or host tensors
-    (streamed through ``streamer``; one is created when omitted). Returns
-    (GradientSet aliasing the accumulator, MiniBatchStats).
+    (streamed through ``streamer``; one is created when omitted). ``tracer``:
+    a ``streaming.ScheduleTracer`` recording the real per-micro schedule.
+    Returns (GradientSet aliasing the accumulator, MiniBatchStats).
     """
     x, y = _as_tensor(x), _as_tensor(y)
     if x.shape[0] != plan.n_b:
@@ -530,26 +552,31 @@ def mini_batch_gradient(model: torch.nn.Module, params: ParameterSet, x, y, plan
     if x.device.type == "cpu" and streamer is None:
         streamer = own_streamer = make_streamer(x, y, plan.n_mu)
     jobs = [(None, lo, hi - lo) for lo, hi in plan.index_ranges]
+    dest = _graph_dest(model, acc, loss_kind, autocast_dtype, loss_from_logits, dice_smoothing, normalize_via)
     try:
-        source = _micro_source(x, y, jobs, staging, prefetch, streamer)
+        source = _micro_source(x, y, jobs, staging, prefetch, streamer, dest, tracer)
         outputs = _run_micro_loop(model, acc, plan, source, normalization, loss_kind, loss_from_logits,
-                                      dice_smoothing, normalize_via, autocast_dtype, keep_outputs)
+                                  dice_smoothing, normalize_via, autocast_dtype, keep_outputs, tracer)
     finally:
         if own_streamer is not None:
             own_streamer.close()
+    if tracer is not None:
+        tracer.update_begin()
     stats_dev = acc.finalize(plan.n_b)
+    if tracer is not None and _close_trace:
+        tracer.update_end()
     stats = MiniBatchStats(stats_dev, plan.n_s_mu, acc.max_micro, outputs)
     return acc.as_gradient_set(), stats
 
 
 def _run_micro_loop(model, acc, plan, source, normalization, loss_kind, loss_from_logits, dice_smoothing,
-                        normalize_via, autocast_dtype, keep_outputs):
+                    normalize_via, autocast_dtype, keep_outputs, tracer=None):
     """The micro loop; K1 records (raw loss, factor, size_k) per micro for the stats."""
     outputs = []
     ctx = torch.autocast("cuda", dtype=autocast_dtype) if autocast_dtype is not None else nullcontext()
     with weight_cast_cache(autocast_dtype):
         return _micro_loop_body(model, acc, plan, source, normalization, loss_kind, loss_from_logits,
-                                dice_smoothing, normalize_via, ctx, keep_outputs, outputs, autocast_dtype)
+                                dice_smoothing, normalize_via, ctx, keep_outputs, outputs, autocast_dtype, tracer)
 
 
 def weight_cast_cache(autocast_dtype):
@@ -569,24 +596,30 @@ def weight_cast_cache(autocast_dtype):
 
 
 def _micro_loop_body(model, acc, plan, source, normalization, loss_kind, loss_from_logits, dice_smoothing,
-                     normalize_via, ctx, keep_outputs, outputs, autocast_dtype=None):
+                     normalize_via, ctx, keep_outputs, outputs, autocast_dtype=None, tracer=None):
     k = -1
     for k, (xk, yk) in enumerate(source):
         if k >= plan.n_s_mu:
             raise AccumulatorOverflowError("source yielded more micro-batches than the plan")
         factor = normalization_factor(plan, k, normalization)
+        if tracer is not None:
+            tracer.micro_begin(k)
         g = _graph_for(model, acc, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing,
                        normalize_via, keep_outputs)
         if g is not None:                 # CUDA-graph replay of fwd + loss + bwd; K1 outside the graph
-            loss = g.replay(xk, yk)
+            loss = g.replay(xk, yk, between=tracer.forward_end if tracer is not None else None)
             acc.add_pointer_table(g.ptrs, factor, loss=loss, loss_factor=factor, loss_weight=float(plan.sizes[k]),
                                   last=(k == plan.n_s_mu - 1))
+            if tracer is not None:
+                tracer.micro_end()
             if keep_outputs:
                 outputs.append(g.out.clone())   # the static output is overwritten by the next replay
             continue
         with ctx:
             out = model(xk)
             loss = compute_loss(loss_kind, out, yk, from_logits=loss_from_logits, dice_smoothing=dice_smoothing)
+        if tracer is not None:
+            tracer.forward_end()
         if normalize_via == "seed":
             loss.backward(torch.full_like(loss, factor))
             kscale = 1.0
@@ -598,6 +631,8 @@ def _micro_loop_body(model, acc, plan, source, normalization, loss_kind, loss_fr
             kscale = factor
         acc.add_module_grads(kscale, loss=loss, loss_factor=factor, loss_weight=float(plan.sizes[k]),
                              last=(k == plan.n_s_mu - 1))
+        if tracer is not None:
+            tracer.micro_end()
         if keep_outputs:
             outputs.append(out.detach())
     if k + 1 != plan.n_s_mu:
@@ -606,7 +641,9 @@ def _micro_loop_body(model, acc, plan, source, normalization, loss_kind, loss_fr
 
 
 CUDA_GRAPHS = os.environ.get("MBS_CUDA_GRAPHS", "1") != "0"
-_NO_GRAPH: set = set()
+# model -> the micro-step shapes whose capture failed (weak keys: a collected model's entry goes with it,
+# and a failure for one shape, e.g. an HBM-filling ragged tail, does not disable the others)
+_NO_GRAPH: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
 def _graph_for(model, acc, loss_kind, xk, yk, autocast_dtype, loss_from_logits, dice_smoothing, normalize_via,
@@ -614,12 +651,16 @@ def _graph_for(model, acc, loss_kind, xk, yk, autocast_dtype, loss_from_logits, 
     """The captured micro step for this micro-batch shape, or None to run eagerly.
 
     Graphs need: CUDA inputs, training mode, the factor applied by K1 (normalize_via "fused") and
-    fp32 gradients in the parameters' memory order (kept outputs are cloned from the static output). A model whose capture fails
-    runs eagerly from then on (the failure is kept, not retried every micro-batch)."""
+    gradients in the parameters' memory order (kept outputs are cloned from the static output). A shape whose
+    capture fails runs eagerly from then on (the failure is kept per model and shape, not retried every
+    micro-batch)."""
     if not (CUDA_GRAPHS and normalize_via == "fused" and model.training
             and isinstance(xk, torch.Tensor) and xk.is_cuda and isinstance(yk, torch.Tensor) and yk.is_cuda):
         return None
-    if id(model) in _NO_GRAPH:
+    shape_key = (tuple(xk.shape), xk.dtype, tuple(yk.shape), yk.dtype, loss_kind, autocast_dtype,
+                 bool(loss_from_logits), float(dice_smoothing))
+    failed = _NO_GRAPH.get(model)
+    if failed is not None and shape_key in failed:
         return None
     from . import graphs
     try:
@@ -629,11 +670,11 @@ def _graph_for(model, acc, loss_kind, xk, yk, autocast_dtype, loss_from_logits, 
         import warnings
         if not isinstance(e, MemoryError):
             warnings.warn(f"CUDA-graph capture of the micro step failed ({type(e).__name__}: {e}); running eagerly")
-        _NO_GRAPH.add(id(model))
+        _NO_GRAPH.setdefault(model, set()).add(shape_key)
         torch.cuda.empty_cache()          # nothing of a failed capture may crowd the eager path
         return None
     if not acc.graph_grads_ok(g.grads):
-        _NO_GRAPH.add(id(model))
+        _NO_GRAPH.setdefault(model, set()).add(shape_key)
         return None
     return g
 
@@ -642,15 +683,22 @@ def train_mini_batch(model: torch.nn.Module, params: ParameterSet, batch: tuple,
                      normalization: str, loss_kind: str, optimizer_state: OptimizerState, *,
                      loss_from_logits: bool = True, dice_smoothing: float = 1.0, prefetch: bool = False,
                      accumulator: GradientAccumulator | None = None,
-                     lr_for_step: Callable[[int], float] | None = None, **kw) -> tuple:
+                     lr_for_step: Callable[[int], float] | None = None, tracer=None, **kw) -> tuple:
     """Stream micro-batches, then update once (engine.py:233-261)."""
     x, y = batch
     total, stats = mini_batch_gradient(model, params, x, y, plan, normalization, loss_kind,
                                        loss_from_logits=loss_from_logits, dice_smoothing=dice_smoothing,
-                                       prefetch=prefetch, accumulator=accumulator, **kw)
+                                       prefetch=prefetch, accumulator=accumulator, tracer=tracer,
+                                       _close_trace=False, **kw)
+    # The reference raises NonFiniteError in the forward, before any update (nn.py:578-579): resolve the
+    # mini-batch's device statistics (one D2H, one host wait per mini-batch) BEFORE the step, so neither the
+    # parameters nor step_count / the LR schedule move on a non-finite mini-batch.
+    stats.resolve()
     if lr_for_step is not None:
         optimizer_state.lr = lr_for_step(optimizer_state.step_count)
     apply_update(params, total, optimizer_state)
+    if tracer is not None:
+        tracer.update_end()
     stats.step_count = optimizer_state.step_count
     return params, stats
 
@@ -663,7 +711,7 @@ def train_epoch(model: torch.nn.Module, params: ParameterSet, x, y, *, mini_batc
                 metric_fn: Callable | None = None, keep_mini_stats: bool = False,
                 accumulator: GradientAccumulator | None = None, staging: Staging | None = None,
                 autocast_dtype: torch.dtype | None = None, streamer: MicroBatchStreamer | None = None,
-                normalize_via: str = "fused") -> EpochStats:
+                normalize_via: str = "fused", tracer=None) -> EpochStats:
     """One pass over the dataset in the reference's deterministic shuffled order (engine.py:276-335).
 
     The whole epoch's micro-batch sequence (mini-batch m = order[m*M:(m+1)*M],
@@ -702,27 +750,31 @@ def train_epoch(model: torch.nn.Module, params: ParameterSet, x, y, *, mini_batc
         max_rows = max(p.n_mu for _, _, p in minis)
         streamer = own_streamer = make_streamer(x, y, max_rows)
     model.train()
-    source = iter(_micro_source(x, y, jobs, staging, prefetch, streamer))
+    dest = _graph_dest(model, acc, loss_kind, autocast_dtype, loss_from_logits, dice_smoothing, normalize_via)
+    source = iter(_micro_source(x, y, jobs, staging, prefetch, streamer, dest, tracer))
     mini_sizes, all_stats, mini_metrics = [], [], []
     try:
         for start, idx, plan in minis:
             acc.begin(plan.n_s_mu)
             outputs = _run_micro_loop(model, acc, plan, _take(source, plan.n_s_mu), normalization, loss_kind,
                                       loss_from_logits, dice_smoothing, normalize_via, autocast_dtype,
-                                      keep_outputs=metric_fn is not None or keep_mini_stats)
+                                      keep_outputs=metric_fn is not None or keep_mini_stats, tracer=tracer)
+            if tracer is not None:
+                tracer.update_begin()
             stats_dev = acc.finalize(plan.n_b)
             stats = MiniBatchStats(stats_dev, plan.n_s_mu, acc.max_micro, outputs)
+            stats.resolve()     # NonFiniteError before the update, as the reference (nn.py:578-579)
             if lr_for_step is not None:
                 optimizer_state.lr = lr_for_step(optimizer_state.step_count)
             apply_update(params, acc.as_gradient_set(), optimizer_state)
+            if tracer is not None:
+                tracer.update_end()
             stats.step_count = optimizer_state.step_count
             mini_sizes.append(len(idx))
             if metric_fn is not None:
                 yb = y[torch.from_numpy(idx.astype(np.int64)).to(y.device)] if on_device else \
                     y[torch.from_numpy(idx.astype(np.int64))]
                 mini_metrics.append(float(metric_fn(stats.outputs, yb.to(stats.outputs.device))))
-            if all_stats:
-                all_stats[-1].resolve()  # one mini-batch behind: surfaces NonFiniteError without stalling
             all_stats.append(stats)
             if not keep_mini_stats:
                 stats._outputs = []

@@ -36,6 +36,7 @@ def _check_same_shape(output, target, kind):
 def mse(output: torch.Tensor, target: torch.Tensor) -> torch.Tensor:
     """losses.py:72-75: mean((o-t)^2); grad 2(o-t)/size."""
     _check_same_shape(output, target, "mse")
+    output = output.float() if output.dtype in (torch.bfloat16, torch.float16) else output
     d = output - target.to(output.dtype)
     return (d * d).mean()
 
@@ -57,6 +58,7 @@ def bce_logits(z: torch.Tensor, target: torch.Tensor) -> torch.Tensor:
 
 def bce_probs(p: torch.Tensor, target: torch.Tensor) -> torch.Tensor:
     """losses.py:90-95: clamp to [1e-12, 1-1e-12]; zero gradient outside the clamp."""
+    p = p.float() if p.dtype in (torch.bfloat16, torch.float16) else p
     c = p.clamp(PROB_CLAMP, 1.0 - PROB_CLAMP)
     t = target.to(p.dtype)
     return -(t * torch.log(c) + (1.0 - t) * torch.log1p(-c)).mean()
@@ -73,7 +75,9 @@ def dice_soft(p: torch.Tensor, target: torch.Tensor, smoothing: float) -> torch.
 
 def compute_loss(kind: str, output: torch.Tensor, target: torch.Tensor, *, from_logits: bool = True,
                  dice_smoothing: float = 1.0) -> torch.Tensor:
-    """Training-loop dispatch (losses.py:184-207). Returns a 0-d device tensor."""
+    """Training-loop dispatch (losses.py:184-207). Returns a 0-d device tensor, always computed and
+    returned in fp32 (or fp64) even when the model output is bf16/fp16 (autocast): the 1e-12 clamp of
+    ``bce`` and the mean reductions need it, and K1 reads the loss as fp32."""
     if kind == "mse":
         return mse(output, target)
     if kind == "cross_entropy":

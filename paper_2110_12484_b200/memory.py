@@ -122,10 +122,11 @@ def measure_budget(model: torch.nn.Module, make_batch, loss_kind: str, *, optimi
 def bn_safe_micro_batch(n_b: int, n_mu: int) -> int:
     """Largest micro-batch size <= n_mu whose plan (engine.py:56-78) has no 1-sample micro-batch.
 
-    The reference allows a 1-sample tail (e.g. 33/16 -> [16, 16, 1]); torch's
-    BatchNorm cannot train on one sample when a channel then holds a single
-    value (BatchNorm1d, or 1x1 spatial maps). The auto-sizer applies this guard
-    to BN models; the plan itself is never altered.
+    The reference allows a 1-sample tail (e.g. 33/16 -> [16, 16, 1]; eps-guarded BatchNorm).
+    K5 (``bn.MicroBatchNorm2d``) follows the reference there, but torch's stock BatchNorm raises when a
+    channel then holds a single value (BatchNorm1d, or 1x1 spatial maps). ``auto_micro_batch`` applies
+    this guard for models that still contain stock torch BatchNorm layers; the plan of a given
+    (n_b, n_mu) is never altered.
     """
     if n_b < 1 or n_mu < 1:
         raise ValueError("batch sizes must be positive")
@@ -135,3 +136,20 @@ def bn_safe_micro_batch(n_b: int, n_mu: int) -> int:
     while m > 1 and n_b % m == 1:
         m -= 1
     return m
+
+
+def has_stock_batchnorm(model: torch.nn.Module) -> bool:
+    """Whether a training-mode forward may run torch's own BatchNorm (which rejects 1-value channels)."""
+    from .bn import MicroBatchNorm2d
+    return any(isinstance(m, torch.nn.modules.batchnorm._BatchNorm) and not isinstance(m, MicroBatchNorm2d)
+               for m in model.modules())
+
+
+def auto_micro_batch(budget: MemoryBudget, n_b: int, model: torch.nn.Module | None = None) -> int:
+    """The micro-batch for a mini-batch of ``n_b``: ``fit_micro_batch`` (memory.py:88-101) capped at n_b,
+    then, for models with stock torch BatchNorm, the largest size <= that with no 1-sample micro-batch
+    (``bn_safe_micro_batch``)."""
+    n = min(fit_micro_batch(budget), int(n_b))
+    if model is not None and has_stock_batchnorm(model):
+        n = bn_safe_micro_batch(int(n_b), n)
+    return n

@@ -62,17 +62,22 @@ def _stream_ptr(stream=None) -> int:
 
 
 def stage_rows(src: torch.Tensor | int, src_dtype: torch.dtype, sample_shape: tuple, rows, row0: int, n: int,
-               staging: Staging, device, stream=None) -> torch.Tensor:
+               staging: Staging, device, stream=None, out: torch.Tensor | None = None) -> torch.Tensor:
     """K2: gather ``n`` rows (device ``rows`` tensor or ``row0..``) of ``src``, cast and lay out.
 
     ``src`` is a device tensor or a raw device/pinned pointer holding NCHW
-    samples of ``src_dtype``.
+    samples of ``src_dtype``. ``out``: a preallocated destination of the
+    staged shape, dtype and layout (e.g. a captured micro step's static input,
+    so the staged bytes are not copied a second time).
     """
     if src_dtype not in (torch.uint8, torch.float32, torch.float64):
         raise ValueError(f"staging supports uint8/float32/float64 sources, got {src_dtype}")
     if staging.dtype not in (torch.float32, torch.bfloat16, torch.float16):
         raise ValueError(f"staging produces float32/bfloat16/float16, got {staging.dtype}")
-    out = staging.out_tensor(n, sample_shape, device)
+    if out is None:
+        out = staging.out_tensor(n, sample_shape, device)
+    elif not _fits(out, staging, (n,) + tuple(sample_shape)):
+        raise ValueError("stage_rows: `out` does not have the staged shape / dtype / layout")
     C, H, W = _chw(sample_shape)
     layout = N.NHWC if (staging.channels_last and len(sample_shape) == 3) else N.NCHW
     src_ptr = src if isinstance(src, int) else src.data_ptr()
@@ -88,9 +93,12 @@ def stage_rows(src: torch.Tensor | int, src_dtype: torch.dtype, sample_shape: tu
 
 
 def gather_rows(src: torch.Tensor | int, dtype: torch.dtype, sample_shape: tuple, rows, row0: int, n: int, device,
-                stream=None) -> torch.Tensor:
-    """Byte-exact row gather of targets (labels, masks) into a fresh device tensor."""
-    out = torch.empty((n,) + tuple(sample_shape), dtype=dtype, device=device)
+                stream=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Byte-exact row gather of targets (labels, masks) into a fresh (or the given contiguous) device tensor."""
+    if out is None:
+        out = torch.empty((n,) + tuple(sample_shape), dtype=dtype, device=device)
+    elif out.dtype != dtype or tuple(out.shape) != (n,) + tuple(sample_shape) or not out.is_contiguous():
+        raise ValueError("gather_rows: `out` does not have the gathered shape / dtype")
     row_bytes = int(np.prod(sample_shape)) * out.element_size() if sample_shape else out.element_size()
     src_ptr = src if isinstance(src, int) else src.data_ptr()
     rows_ptr = rows.data_ptr() if rows is not None else None
@@ -101,19 +109,47 @@ def gather_rows(src: torch.Tensor | int, dtype: torch.dtype, sample_shape: tuple
     return out
 
 
-def device_micro_batches(x: torch.Tensor, y: torch.Tensor, jobs, staging: Staging | None):
-    """Device-resident source: yields (xk, yk) for each (rows, row0, n) job."""
+def _fits(t: torch.Tensor, staging: Staging, shape: tuple) -> bool:
+    if t.dtype != staging.dtype or tuple(t.shape) != tuple(shape):
+        return False
+    if staging.channels_last and len(shape) == 4:
+        return t.is_contiguous(memory_format=torch.channels_last)
+    return t.is_contiguous()
+
+
+def _dest(dest, n, sample_shape, staging, y_shape, y_dtype):
+    """The consumer's preallocated (x, y) buffers for a micro-batch of n rows, or None."""
+    if dest is None:
+        return None
+    return dest((n,) + tuple(sample_shape), staging.dtype, staging.channels_last and len(sample_shape) == 3,
+                (n,) + tuple(y_shape), y_dtype)
+
+
+def device_micro_batches(x: torch.Tensor, y: torch.Tensor, jobs, staging: Staging | None, *, dest=None,
+                         tracer=None):
+    """Device-resident source: yields (xk, yk) for each (rows, row0, n) job.
+
+    ``dest(x_shape, x_dtype, channels_last, y_shape, y_dtype) -> (x_buf, y_buf) | None`` lets the consumer
+    name where a staged micro-batch goes (a captured micro step's static buffers); ``tracer`` marks the
+    point each micro-batch's data is ready (``streaming.ScheduleTracer``)."""
     dev = x.device
+    st = staging or Staging(dtype=x.dtype if x.is_floating_point() and x.dtype != torch.float64
+                            else torch.float32)
     for rows, row0, n in jobs:
+        if tracer is not None:
+            tracer.data_ready()
         if rows is None and (staging is None or staging.is_identity_for(x)):
             xk = x[row0:row0 + n]
             yk = y[row0:row0 + n]
         else:
-            st = staging or Staging(dtype=x.dtype if x.is_floating_point() and x.dtype != torch.float64
-                                    else torch.float32)
-            xk = stage_rows(x, x.dtype, tuple(x.shape[1:]), rows, row0, n, st, dev)
-            yk = (gather_rows(y, y.dtype, tuple(y.shape[1:]), rows, row0, n, dev) if rows is not None
-                  else y[row0:row0 + n])
+            buf = _dest(dest, n, tuple(x.shape[1:]), st, tuple(y.shape[1:]), y.dtype)
+            xk = stage_rows(x, x.dtype, tuple(x.shape[1:]), rows, row0, n, st, dev,
+                            out=buf[0] if buf is not None else None)
+            if rows is not None:
+                yk = gather_rows(y, y.dtype, tuple(y.shape[1:]), rows, row0, n, dev,
+                                 out=buf[1] if buf is not None else None)
+            else:
+                yk = y[row0:row0 + n]
         yield xk, yk
 
 
@@ -147,6 +183,7 @@ class MicroBatchStreamer:
         self.dev_slots = [torch.empty(self.slot_bytes, dtype=torch.uint8, device=self.device)
                           for _ in range(self.n_slots)]
         self.jobs_issued: list = []   # (job_seq, n_rows) not yet harvested
+        self.slot_job = [-1] * self.n_slots
         self._harvested: list = []    # (gather_ms, copy_ms, blocked_ms, bytes) of older jobs
 
     def close(self):
@@ -177,12 +214,20 @@ class MicroBatchStreamer:
         N.check(N.lib().mbs_streamer_submit(self._h, slot, parts, 2, rows_ptr, int(row0), int(n),
                                             ctypes.byref(job)), "mbs_streamer_submit")
         self.jobs_issued.append((job.value, n))
+        self.slot_job[slot] = job.value
         if len(self.jobs_issued) > 128:       # harvest long-finished jobs before the native ring (256) wraps
             old, self.jobs_issued = self.jobs_issued[:64], self.jobs_issued[64:]
             self._harvested.extend(self._read_timings(old))
 
-    def stream(self, x: torch.Tensor, y: torch.Tensor, jobs, staging: Staging | None, *, prefetch: bool = True):
-        """Yield (xk, yk) device tensors for each (rows, row0, n) job over host tensors x, y."""
+    def timeline(self, job: int, origin: torch.cuda.Event) -> tuple:
+        """(copy start, copy end) of job ``job``, seconds after ``origin`` (copy-stream events)."""
+        from .streaming import streamer_timeline
+        return streamer_timeline(self._h, job, origin)
+
+    def stream(self, x: torch.Tensor, y: torch.Tensor, jobs, staging: Staging | None, *, prefetch: bool = True,
+               dest=None, tracer=None):
+        """Yield (xk, yk) device tensors for each (rows, row0, n) job over host tensors x, y
+        (``dest`` / ``tracer``: see ``device_micro_batches``)."""
         if x.device.type != "cpu" or y.device.type != "cpu":
             raise ValueError("MicroBatchStreamer streams host-resident tensors")
         if not (x.is_contiguous() and y.is_contiguous()):
@@ -205,9 +250,14 @@ class MicroBatchStreamer:
                 self._submit(slot, x, y, *jobs[k])
                 nxt += 1
             N.check(N.lib().mbs_streamer_wait(self._h, slot, cs.cuda_stream), "mbs_streamer_wait")
+            if tracer is not None:
+                tracer.data_ready(self.slot_job[slot], self, cs)
             base = self.dev_slots[slot].data_ptr()
-            xk = stage_rows(base, x.dtype, sample_shape, None, 0, n, staging, self.device, cs)
-            yk = gather_rows(base + self.y_off, y.dtype, y_shape, None, 0, n, self.device, cs)
+            buf = _dest(dest, n, sample_shape, staging, y_shape, y.dtype)
+            xk = stage_rows(base, x.dtype, sample_shape, None, 0, n, staging, self.device, cs,
+                            out=buf[0] if buf is not None else None)
+            yk = gather_rows(base + self.y_off, y.dtype, y_shape, None, 0, n, self.device, cs,
+                             out=buf[1] if buf is not None else None)
             N.check(N.lib().mbs_streamer_release(self._h, slot, cs.cuda_stream), "mbs_streamer_release")
             if prefetch and nxt < len(jobs):
                 self._submit(nxt % self.n_slots, x, y, *jobs[nxt])

@@ -119,17 +119,25 @@ def build_model(w: Workload, ops: str = "torch") -> nn.Module:
     else:
         raise ValueError(w.model)
     if ops == "native":
-        from .bn import fuse_batchnorm
-        from .pool import swap_maxpool
-        from .stem import swap_pointwise, swap_stem
-        fuse_batchnorm(m)
-        swap_maxpool(m)
-        swap_stem(m)
-        swap_pointwise(m)
-        if isinstance(m, UNet):
-            m.native_skips = True
+        make_native(m)
     elif ops != "torch":
         raise ValueError(f"ops must be 'native' or 'torch', got {ops!r}")
+    return m
+
+
+def make_native(m: nn.Module) -> nn.Module:
+    """Route a stock model's BatchNorm(+ReLU/+skip add), max-pools, 3-channel stem conv and narrow 1x1
+    head onto K5/K6/K7 in place (class swaps only: parameter names, order and values are unchanged,
+    so the stock module and its native twin share one oracle)."""
+    from .bn import fuse_batchnorm
+    from .pool import swap_maxpool
+    from .stem import swap_pointwise, swap_stem
+    fuse_batchnorm(m)
+    swap_maxpool(m)
+    swap_stem(m)
+    swap_pointwise(m)
+    if isinstance(m, UNet):
+        m.native_skips = True
     return m
 
 

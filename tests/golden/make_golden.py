@@ -130,6 +130,10 @@ MODELS = {
                 12, 5, "adam"),
     "seg_bce_dice": ([nn.Conv2d(2, 4, 3, 1, 1), nn.Relu(), nn.Conv2d(4, 1, 3, 1, 1)], (2, 6, 6),
                      "bce_dice", "mask", 7, 3, "adam"),
+    # a 1x1 feature map into BatchNorm with a 1-sample tail micro-batch (9/4 -> [4, 4, 1]): one value per
+    # channel, legal in the reference (eps-guarded; biased running variance nn.py:329-332)
+    "bn1_tail": ([nn.Conv2d(3, 4, 4, 1, 0), nn.BatchNorm(4), nn.Relu(), nn.Flatten(), nn.Dense(4, 5)],
+                 (3, 4, 4), "cross_entropy", "classes5", 9, 4, "sgd"),
 }
 
 

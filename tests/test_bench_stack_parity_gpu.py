@@ -1,0 +1,163 @@
+"""The EXACT benchmarked stack against the float64 oracle, at the BASELINE configs' model shapes.
+
+bench.py trains with: the native model ops (K5 BatchNorm(+ReLU/+skip add), K6 max-pool / U-Net skip
+join, K7 stem), channels_last, uint8 inputs staged by K2 to NHWC, CUDA-graph replay of the micro
+step, K1 accumulation and K3 step — in two precisions:
+
+* ``bf16``: ``ParameterSet(shadow=bf16)`` (bf16 weights written by K3, bf16 weight gradients widened
+  by K1), bf16 staging, bf16 autocast;
+* ``fp32``: fp32 weights and staging, no autocast, TF32 off.
+
+The oracle is oracle/hybrid.py: the same stock module in float64 on the CPU per micro-batch,
+seeded exactly as ``backward(tape, factor)`` (engine.py:214-215 -> nn.py:596), accumulated /
+normalised / stepped by the float64 restatement of engine.py / optim.py.
+
+Tolerance: the model numerics of a precision have a floor against float64
+that is not an MBS property. It is measured in each case as PLAIN torch on this GPU at the same
+precision (stock modules, torch autocast casting fp32 masters for bf16), the same micro split and
+factors, autograd accumulation. Contract, per precision:
+
+    accumulated gradient   rel-L2(ours, fp64) <= max(1e-5, 1.5 * rel-L2(plain, fp64))
+    loss / grad-norm       |rel err| <= max(1e-5, 1.5 * plain's) (+ 1e-6 slack)
+    post-step weights      rel-L2(ours, fp64) <= max(1e-5, 1.5 * the same step's floor)
+    the step itself        fp64 optimizer applied to OUR gradient == our K3 result to 1e-6
+
+Shapes (reduced N_B, same micro size / tail structure where the full N_B would not run on a CPU):
+C1 exactly (ResNet-18@32, 64/8), ResNet-50@224 102 classes 20/8 -> [8, 8, 4], U-Net@384 6/4 ->
+[4, 2] (bce_dice + Adam). Per-tensor errors go to ``$MBS_PARITY_REPORT`` (JSON lines) when set.
+"""
+import copy
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2110_12484_b200 as mbs
+from oracle import mbs_oracle as O
+from oracle.hybrid import TorchGradFn
+from paper_2110_12484_b200 import graphs
+from paper_2110_12484_b200.streamer import Staging
+from paper_2110_12484_b200.workloads import WORKLOADS, build_model, make_native
+from tests.gpu_util import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "c1_resnet18_64_8": ("c1", 64, 8, (3, 32, 32)),
+    "c2_resnet50_224_20_8": ("c2", 20, 8, (3, 224, 224)),
+    "c3_unet_384_6_4": ("c3", 6, 4, (3, 384, 384)),
+}
+
+
+def _flat(d, names):
+    return np.concatenate([np.asarray(d[n], np.float64).ravel() for n in names])
+
+
+def _data(w, n, shape, seed):
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randint(0, 256, (n,) + shape, dtype=torch.uint8, generator=g)
+    if w.target == "classes":
+        y = torch.randint(0, w.n_classes, (n,), generator=g)
+    else:
+        y = (torch.rand((n, 1) + shape[1:], generator=g) < 0.5).float()
+    return x, y
+
+
+def _opt(kind, ours: bool):
+    if kind == "sgd":
+        return mbs.sgd_state(0.01, 0.9, 5e-4) if ours else O.OptState("sgd", 0.01, 0.9, 5e-4)
+    return mbs.adam_state(0.01, 5e-4) if ours else O.OptState("adam", 0.01, weight_decay=5e-4)
+
+
+def _plain_gpu(cuda, net, w, x, y, plan, mode, precision):
+    """Stock torch on this GPU at the precision: the floor of the model numerics."""
+    pnet = copy.deepcopy(net).to(cuda).to(memory_format=torch.channels_last).train()
+    ctx = torch.autocast("cuda", dtype=torch.bfloat16) if precision == "bf16" else torch.autocast("cuda",
+                                                                                                   enabled=False)
+    losses = []
+    for k, (lo, hi) in enumerate(plan.index_ranges):
+        f = O.normalization_factor(plan, k, mode)
+        xk = x[lo:hi].to(cuda).float().contiguous(memory_format=torch.channels_last)
+        with ctx:
+            loss = mbs.compute_loss(w.loss_kind, pnet(xk), y[lo:hi].to(cuda))
+        (loss * f).backward()
+        losses.append(float(loss))
+    grads = {n: p.grad.double().cpu().numpy() for n, p in pnet.named_parameters()}
+    return grads, O.mini_loss(plan.sizes, losses, plan.n_b)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("case", list(CASES))
+def test_bench_stack_vs_fp64_oracle(cuda, case, precision):
+    cfg, n_b, n_mu, shape = CASES[case]
+    w = WORKLOADS[cfg]
+    mode = w.normalization
+    torch.manual_seed(0)
+    net = build_model(w, ops="torch").train()
+    x, y = _data(w, n_b, shape, seed=11)
+    plan = O.plan_split(n_b, n_mu)
+
+    # float64 oracle
+    ref = TorchGradFn(net, w.loss_kind)
+    names = ref.names
+    shapes = {n: v.shape for n, v in ref.params().items()}
+    g64, st64 = O.mini_batch_gradient(ref, shapes, x.double().numpy(), y.numpy(), plan, mode)
+
+    # floor: plain torch on this GPU at this precision
+    plain, plain_loss = _plain_gpu(cuda, net, w, x, y, plan, mode, precision)
+    floor = rel_l2(_flat(plain, names), _flat(g64, names))
+
+    # ours: exactly bench.py's stack
+    graphs.clear()
+    dnet = make_native(copy.deepcopy(net)).to(cuda).to(memory_format=torch.channels_last)
+    bf16 = precision == "bf16"
+    params = mbs.ParameterSet(dnet, shadow=torch.bfloat16 if bf16 else None)
+    staging = Staging(dtype=torch.bfloat16 if bf16 else torch.float32, channels_last=True)
+    total, st = mbs.mini_batch_gradient(dnet, params, x.to(cuda), y.to(cuda), mbs.plan_split(n_b, n_mu), mode,
+                                        w.loss_kind, staging=staging,
+                                        autocast_dtype=torch.bfloat16 if bf16 else None)
+    assert graphs._CACHE, "the micro step did not run from a CUDA graph (bench.py's path)"
+    got = {n: total[n].detach().double().cpu().numpy() for n in names}
+    err = rel_l2(_flat(got, names), _flat(g64, names))
+    loss_err = abs(st.loss - st64["loss"]) / abs(st64["loss"])
+    loss_floor = abs(plain_loss - st64["loss"]) / abs(st64["loss"])
+    gn_err = abs(st.grad_norm - st64["grad_norm"]) / st64["grad_norm"]
+    gn_floor = abs(np.linalg.norm(_flat(plain, names)) - st64["grad_norm"]) / st64["grad_norm"]
+
+    # one optimizer step from the same start
+    w0 = ref.params()
+    w64 = {n: v.copy() for n, v in w0.items()}
+    O.apply_update(w64, g64, _opt(w.optimizer, False))
+    wpl = {n: v.copy() for n, v in w0.items()}
+    O.apply_update(wpl, plain, _opt(w.optimizer, False))
+    wfloor = rel_l2(_flat(wpl, names), _flat(w64, names))
+    wo = {n: v.copy() for n, v in w0.items()}
+    O.apply_update(wo, got, _opt(w.optimizer, False))       # the float64 step on OUR gradient
+    dst = _opt(w.optimizer, True)
+    mbs.apply_update(params, total, dst)
+    wg = {n: params[n].detach().double().cpu().numpy() for n in names}
+    werr = rel_l2(_flat(wg, names), _flat(w64, names))
+    step_err = rel_l2(_flat(wg, names), _flat(wo, names))
+    if bf16:   # the shadow the next forward reads is the RNE cast of the updated master
+        assert torch.equal(params.shadow, params.flat.to(torch.bfloat16))
+
+    per_tensor = {n: {"ours": rel_l2(got[n], g64[n]), "plain": rel_l2(plain[n], g64[n])} for n in names}
+    worst = max(names, key=lambda n: per_tensor[n]["ours"])
+    rep = {"case": case, "precision": precision, "plan": list(plan.sizes), "grad_rel_l2": err,
+           "grad_floor": floor, "ratio": err / floor if floor else None, "loss_rel": loss_err,
+           "loss_floor": loss_floor, "grad_norm_rel": gn_err, "grad_norm_floor": gn_floor,
+           "post_step_rel_l2": werr, "post_step_floor": wfloor, "k3_step_vs_fp64_step": step_err,
+           "worst_tensor": worst, "per_tensor": per_tensor}
+    path = os.environ.get("MBS_PARITY_REPORT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rep) + "\n")
+    graphs.clear()
+
+    assert err <= max(1e-5, 1.5 * floor), rep
+    assert loss_err <= max(1e-5, 1.5 * loss_floor) + 1e-6, rep
+    assert gn_err <= max(1e-5, 1.5 * gn_floor) + 1e-6, rep
+    assert step_err <= 1e-6, rep
+    assert werr <= max(1e-5, 1.5 * wfloor), rep

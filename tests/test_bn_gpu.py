@@ -145,10 +145,23 @@ def test_k5_nchw_input_is_converted(cuda):
         assert rel_l2(got[k].double().cpu().numpy(), want[k].cpu().numpy()) <= 1e-5, k
 
 
-def test_k5_size_one_micro_batch_raises_like_torch(cuda):
+def test_k5_one_value_per_channel_follows_the_reference(cuda):
+    """One value per channel (a 1-sample micro-batch on a 1x1 map): torch raises, the reference does not
+    (SPEC.md:92). K5: y = beta (+ReLU), dx = 0, dbeta = sum dy, dgamma = 0, running_var -> biased 0."""
     m = K5.MicroBatchNorm2d(8).to(cuda).train()
-    with pytest.raises(ValueError, match="more than 1 value per channel"):
-        m(torch.randn(1, 8, 1, 1, device=cuda))
+    with torch.no_grad():
+        m.weight.uniform_(0.5, 1.5)
+        m.bias.uniform_(-1.0, 1.0)
+    x = torch.randn(1, 8, 1, 1, device=cuda, requires_grad=True)
+    y = m(x)
+    assert torch.equal(y.detach().reshape(8), m.bias.detach())
+    dy = torch.randn_like(y)
+    y.backward(dy)
+    assert torch.count_nonzero(x.grad) == 0
+    assert torch.equal(m.bias.grad, dy.reshape(8))
+    assert torch.count_nonzero(m.weight.grad) == 0
+    assert torch.allclose(m.running_mean, 0.1 * x.detach().reshape(8))
+    assert torch.allclose(m.running_var, torch.full((8,), 0.9, device=cuda))
     with pytest.raises(ValueError):
         F.batch_norm(torch.randn(1, 8, 1, 1, device=cuda), None, None, training=True)
 

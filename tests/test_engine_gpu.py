@@ -220,10 +220,36 @@ def test_nonfinite_loss_raises_and_keeps_params(cuda):
     x[2, 0] = float("inf")
     before = params.flat.clone()
     st = mbs.sgd_state()
-    _, stats = mbs.train_mini_batch(mod, params, (x, y), mbs.plan_split(6, 3), "paper_faithful", "mse", st)
+    # the reference raises before any update (nn.py:578-579): parameters, moments and step_count untouched
     with pytest.raises(mbs.NonFiniteError):
-        stats.loss
-    assert torch.equal(params.flat, before)          # the device guard skipped the step
+        mbs.train_mini_batch(mod, params, (x, y), mbs.plan_split(6, 3), "paper_faithful", "mse", st)
+    assert torch.equal(params.flat, before)
+    assert st.step_count == 0 and not st.velocity
+
+
+def test_nonfinite_in_epoch_raises_before_that_mini_batch_step(cuda):
+    """A non-finite sample in mini-batch 2 of an epoch: the exception surfaces with exactly the state the
+    reference leaves (mini-batch 1 stepped, mini-batch 2 not; step_count 1)."""
+    from paper_2110_12484_b200.rng import epoch_order
+    meta = load_json("e2e.json")["mlp_mse"]
+    a = load_npz("e2e.npz")
+    mod, params = _model(meta, a, "mlp_mse", cuda)
+    x, y = _xy(a, "mlp_mse", meta, 0, 12, cuda)
+    order = epoch_order(12, 5, 0, True)
+    x[int(order[6 + 1]), 0] = float("nan")                 # lands in the second mini-batch of 6
+    w0 = params.flat.clone()
+    st = mbs.sgd_state(0.01, 0.9, 0.0)
+    with pytest.raises(mbs.NonFiniteError):
+        mbs.train_epoch(mod, params, x, y, mini_batch_size=6, micro_batch_size=4, normalization="exact_weighted",
+                        loss_kind="mse", optimizer_state=st, seed=5, epoch_index=0)
+    assert st.step_count == 1
+    after_first = params.flat.clone()
+    # the same first step taken alone from the same start
+    params.flat.copy_(w0)
+    st1 = mbs.sgd_state(0.01, 0.9, 0.0)
+    idx = torch.from_numpy(order[:6].astype(np.int64)).to(cuda)
+    mbs.train_mini_batch(mod, params, (x[idx], y[idx]), mbs.plan_split(6, 4), "exact_weighted", "mse", st1)
+    assert torch.equal(params.flat, after_first)
 
 
 def test_cuda_graph_micro_step_matches_eager(cuda, monkeypatch):
@@ -256,3 +282,44 @@ def test_cuda_graph_micro_step_matches_eager(cuda, monkeypatch):
     for k in a[2]:
         assert torch.allclose(a[2][k], b[2][k], rtol=1e-5, atol=1e-6), k
     graphs.clear()
+
+
+@pytest.mark.parametrize("mode", ["paper_faithful", "exact_weighted", "off"])
+def test_bn_one_sample_tail_matches_reference(cuda, mode):
+    """9/4 -> [4, 4, 1] into a BatchNorm over a 1x1 map: the tail micro-batch has ONE value per channel.
+    The reference accepts it; torch's BatchNorm raises; K5 follows the reference: gradients,
+    losses and two post-step weights against the reference's own run (fixture ``bn1_tail``)."""
+    from paper_2110_12484_b200 import bn as K5
+    name = "bn1_tail"
+    meta = load_json("e2e.json")[name]
+    a = load_npz("e2e.npz")
+    torch.manual_seed(0)
+    mod = build_torch(meta["spec"], tuple(meta["input_shape"])).to(cuda)
+    load_ref_params(mod, meta["spec"], {n: a[f"{name}/p0/{n}"] for n in meta["param_names"]})
+    K5.fuse_batchnorm(mod)
+    params = mbs.ParameterSet(mod)
+    n_b = meta["n_b"]
+    plan = mbs.plan_split(n_b, meta["n_mu"])
+    assert plan.sizes == (4, 4, 1)
+    x, y = _xy(a, name, meta, 0, n_b, cuda)
+    total, stats = mbs.mini_batch_gradient(mod, params, x, y, plan, mode, meta["loss_kind"])
+    got = to_ref(meta["spec"], {tn: total[tn] for tn in params.names()})
+    keys = sorted(got)
+    assert rel_l2(np.concatenate([got[k].ravel() for k in keys]),
+                  np.concatenate([a[f"{name}/{mode}/grad0/{k}"].ravel() for k in keys])) <= 1e-5
+    ms = meta["modes"][mode][0]
+    np.testing.assert_allclose(stats.losses_raw, [fhex(v) for v in ms["losses_raw"]], rtol=1e-5)
+    assert stats.loss == pytest.approx(fhex(ms["loss"]), rel=1e-5)
+    # the running statistics of the first mini-batch differ only in the variance convention (documented);
+    # restart from the fixture's start for the two-step trajectory
+    mod2 = build_torch(meta["spec"], tuple(meta["input_shape"])).to(cuda)
+    load_ref_params(mod2, meta["spec"], {n: a[f"{name}/p0/{n}"] for n in meta["param_names"]})
+    K5.fuse_batchnorm(mod2)
+    params2 = mbs.ParameterSet(mod2)
+    st = _opt(meta)
+    for mb in range(2):
+        x, y = _xy(a, name, meta, mb * n_b, (mb + 1) * n_b, cuda)
+        mbs.train_mini_batch(mod2, params2, (x, y), plan, mode, meta["loss_kind"], st)
+        got = to_ref(meta["spec"], {tn: params2[tn] for tn in params2.names()})
+        assert rel_l2(np.concatenate([got[k].ravel() for k in keys]),
+                      np.concatenate([a[f"{name}/{mode}/p{mb + 1}/{k}"].ravel() for k in keys])) <= 1e-5

@@ -1,7 +1,9 @@
-"""memory.fit_micro_batch and streaming.simulate_stream vs the reference's fixtures (CPU)."""
+"""memory.fit_micro_batch vs the reference's fixtures; the oracle's stream simulator vs the reference's
+schedules; the product's schedule shapes / overhead report / overlap fraction (CPU)."""
 import pytest
 
 import paper_2110_12484_b200 as mbs
+from oracle import streaming_sim as S
 from paper_2110_12484_b200 import memory, streaming
 from tests.golden_io import load_json
 
@@ -21,26 +23,45 @@ def test_fit_micro_batch_golden():
 
 
 def test_simulate_stream_golden():
+    """The oracle's virtual-time simulator (test infrastructure) == the reference's own schedules."""
     for case in load_json("misc.json")["simulate_stream"]:
-        plan = mbs.plan_split(case["n_b"], case["n_mu"])
-        cost = streaming.CostModel(*case["cost"])
-        s = streaming.simulate_stream(plan, cost, case["bps"], overlap=case["overlap"])
-        assert s.makespan.hex() == case["makespan"]
-        assert [[e.kind, e.index, e.start.hex(), e.end.hex()] for e in s.events] == case["events"]
+        sizes = mbs.plan_split(case["n_b"], case["n_mu"]).sizes
+        cost = S.CostModel(*case["cost"])
+        makespan, events = S.simulate_stream(sizes, cost, case["bps"], overlap=case["overlap"])
+        assert makespan.hex() == case["makespan"]
+        assert [[e[0], e[1], e[2].hex(), e[3].hex()] for e in events] == case["events"]
         if not case["overlap"]:
-            assert streaming.sequential_makespan(plan, cost, case["bps"]).hex() == case["makespan"]
+            assert S.sequential_makespan(sizes, cost, case["bps"]).hex() == case["makespan"]
+    with pytest.raises(ValueError):
+        S.CostModel(-1.0, 0.0, 0.0)
 
 
-def test_overhead_report():
-    plan = mbs.plan_split(8, 2)
-    c = streaming.CostModel(1e-3, 1.0, 2.0, 0.5, 0.1, 0.2)
-    a = streaming.simulate_stream(plan, c, 100, overlap=True)
-    b = streaming.simulate_stream(mbs.plan_split(8, 8), c, 100, overlap=False)
+def _sched(events):
+    evs = tuple(streaming.StreamEvent(*e) for e in events)
+    t0 = min(e.start for e in evs)
+    return streaming.StreamSchedule(evs, max(e.end for e in evs) - t0, True)
+
+
+def test_overhead_report_on_schedules():
+    """streaming.py:130-149 applied to two (measured-shape) schedules; a failed baseline is reported."""
+    sizes = mbs.plan_split(8, 2).sizes
+    c = S.CostModel(1e-3, 1.0, 2.0, 0.5, 0.1, 0.2)
+    a = _sched(S.simulate_stream(sizes, c, 100, overlap=True)[1])
+    b = _sched(S.simulate_stream((8,), c, 100, overlap=False)[1])
     r = streaming.overhead_report(a, b)
     assert r.overhead_seconds == pytest.approx(a.makespan - b.makespan)
+    assert r.overhead_pct == pytest.approx(100 * (a.makespan - b.makespan) / b.makespan)
     assert streaming.overhead_report(a, None).baseline_failed
-    m = streaming.measured_schedule([1.0, 1.0, 1.0], [30.0, 30.0, 30.0], 0.5)
-    assert m.makespan == pytest.approx((1.0 + 90.0 + 0.5) / 1e3)
+
+
+def test_overlap_fraction():
+    # transfer 1 hidden behind compute 0; transfer 2 ends 0.5 after compute 1 -> 0.5 of 3.0 exposed
+    s = _sched([("transfer", 0, 0.0, 1.0), ("forward", 0, 1.0, 2.0), ("backward", 0, 2.0, 4.0),
+                ("transfer", 1, 1.0, 2.0), ("forward", 1, 4.0, 5.0), ("backward", 1, 5.0, 7.0),
+                ("transfer", 2, 6.5, 7.5), ("forward", 2, 7.5, 8.0), ("backward", 2, 8.0, 9.0),
+                ("update", -1, 9.0, 9.5)])
+    assert streaming.overlap_fraction(s) == pytest.approx(1.0 - 0.5 / 3.0)
+    assert streaming.overlap_fraction(_sched([("forward", 0, 0.0, 1.0), ("backward", 0, 1.0, 2.0)])) is None
 
 
 def test_bn_safe_micro_batch():
@@ -54,3 +75,17 @@ def test_bn_safe_micro_batch():
             m = bn_safe_micro_batch(n_b, n_mu)
             assert 1 <= m <= n_mu
             assert min(mbs.plan_split(n_b, m).sizes) > 1 or m == 1
+
+
+def test_auto_micro_batch_applies_the_bn_guard_to_stock_batchnorm_only():
+    import torch
+    from paper_2110_12484_b200 import bn
+    b = memory.MemoryBudget(capacity_bytes=1000 + 16 * 10, param_bytes=1000, data_bytes_per_sample=10)
+    assert memory.fit_micro_batch(b) == 16
+    stock = torch.nn.Sequential(torch.nn.Conv2d(3, 4, 3), torch.nn.BatchNorm2d(4))
+    assert memory.auto_micro_batch(b, 33, stock) == 15           # 33/16 -> [16,16,1]: torch BN would raise
+    native = torch.nn.Sequential(torch.nn.Conv2d(3, 4, 3), torch.nn.BatchNorm2d(4))
+    bn.fuse_batchnorm(native)
+    assert memory.auto_micro_batch(b, 33, native) == 16          # K5 takes the 1-sample tail (reference rule)
+    assert memory.auto_micro_batch(b, 8, stock) == 8             # capped at the mini-batch
+    assert memory.auto_micro_batch(b, 33, None) == 16
