@@ -1,35 +1,42 @@
 #!/usr/bin/env python
-"""Benchmark: effective-batch samples/s of Micro-Batch Streaming on B200.
+"""Benchmark: effective-batch samples/s of Micro-Batch Streaming on B200, batch > HBM.
 
-Default workload (BASELINE.json configs[1]): ResNet-50 @224 (102 classes,
-synthetic Flower-102-shaped uint8 images), mini-batch 1024 streamed as
-micro-batch 128, cross-entropy, SGD(0.01, 0.9, 5e-4), exact_weighted
-normalisation. One STEP = one mini-batch: 8 micro-batch forward/backward
-passes (bf16 autocast on cuDNN, fp32 master weights), 8 fused K1
-normalise+accumulate passes, the loss/grad-norm finalize and one fused K3
-optimizer step.
+Default workload (BASELINE.json ``configs[3]``, the config the metric "(batch > HBM)" is quoted on):
+ResNet-50 @224 (102 classes, synthetic Flower-102-shaped uint8 images, random labels, random init),
+ONE mini-batch of 300,032 samples per GPU streamed as 2,344 micro-batches of 128 — 45.2 GB
+host-resident as uint8, 180.6 GB as the reference's float32 arrays (> the 180 GB of HBM) — cross
+entropy, SGD(0.01, 0.9, 5e-4), exact_weighted normalisation. The host dataset is exactly one
+mini-batch; every step is one epoch over it (reshuffled per epoch by ``epoch_index``, engine.py:300).
+One STEP = one mini-batch: 2,344 micro forward/backward passes (bf16 autocast on cuDNN, bf16 shadow
+weights), 2,344 fused K1 normalise+accumulate passes, the loss/grad-norm finalize and one fused K3
+optimizer step. ``--config c2`` is the fits-in-HBM 1024/128 case.
 
-* ``value``  — inputs already resident in HBM (uint8), staged per micro-batch by K2.
-* ``e2e``    — the same API fed from PINNED HOST memory: every step's micro-batches
-  are copied H2D through the streamer inside the timed region, and every
-  step's loss is read back (D2H).
-* ``no_stream`` — plain torch training at batch = micro (128), data resident: the
-  paper's "w/o MBS" run; ``stream_vs_no_stream`` = value / no_stream.
-* ``roofline`` — K1 (the dominant MBS kernel) achieved algorithmic GB/s, timed
-  live with CUDA events on its stream, vs the measured HBM copy peak.
-* ``cpu_baseline`` — the CPU oracle port (float64 torch-CPU model + NumPy MBS
-  arithmetic, the reference's algorithm) on a bounded sample, rank 0, N=1.
+* ``value``   — inputs resident in HBM (uint8), staged per micro-batch by K2.
+* ``e2e``     — the same API fed from PINNED HOST memory: every micro-batch is copied H2D through the
+  streamer inside the timed region and every mini-batch's loss is read back (D2H).
+* ``no_stream`` — plain torch training at batch = micro, data resident (the paper's "w/o MBS" run);
+  ``e2e_vs_no_stream`` is the north-star ratio.
+* ``overhead`` — the reference's overhead report (streaming.py:130-149) on the MEASURED schedule of
+  the timed e2e run (``streaming.ScheduleTracer``: CUDA events per micro-batch on the copy and
+  compute streams), and the H2D overlap fraction from the same events.
+* ``roofline`` — K1 (the accumulate kernel the north star names) achieved algorithmic GB/s, timed live
+  with CUDA events on its stream, vs the measured HBM copy peak.
+* ``precision_fp32`` — the same MBS stack in fp32 (TF32 off), the precision every oracle parity test
+  also pins; context only.
+* ``cpu_baseline`` — the CPU oracle port (float64 torch-CPU model + NumPy MBS arithmetic, the
+  reference's algorithm) on a bounded sample, rank 0, N=1.
 
-``--impl reference`` runs only that CPU reference path (all host threads).
-Multi-GPU (torchrun): each rank streams its own mini-batch of 1024 (weak
-scaling); the global plan's micro-batches are partitioned across ranks and
-one NCCL all-reduce per mini-batch combines the accumulated gradients.
+``--impl reference`` runs only that CPU reference path (all host threads) on the same workload config.
+Multi-GPU (torchrun): each rank streams its own mini-batch (weak scaling); the global plan's
+micro-batches are partitioned across ranks and one NCCL all-reduce per mini-batch combines the
+accumulated gradients.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -42,12 +49,16 @@ import torch
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "effective-batch samples/sec"
+HOST_DATA_CAP = 8 << 30          # host bytes per rank beyond which the dataset is ONE mini-batch
+CPU_SAMPLE = (16, 8)             # the CPU reference's bounded sample: mini 16 streamed as micro 8
+
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback"
 
@@ -67,7 +78,7 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "500"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -107,10 +118,22 @@ class ClockSampler:
 
 
 def _dist():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def workload_config(w, n_b: int, n_mu: int, ws: int, model_ops: str) -> dict:
+    """The ``config`` object of BOTH arms' JSON lines (the workload; what a sample of it ran is separate)."""
+    from paper_2110_12484_b200 import engine
+    plan = engine.plan_split(n_b, n_mu)
+    row = int(np.prod(w.sample_shape))
+    return {"workload": w.name, "model": w.model, "input": "x".join(map(str, w.sample_shape)),
+            "mini_batch_per_gpu": n_b, "micro_batch": n_mu, "n_micro": plan.n_s_mu,
+            "micro_sizes_head_tail": [plan.sizes[0], plan.sizes[-1]], "global_batch": n_b * ws,
+            "parallelism": f"dp{ws}", "normalization": w.normalization, "optimizer": w.optimizer,
+            "loss": w.loss_kind,
+            "mini_batch_bytes": {"uint8": n_b * row, "fp32_as_reference_holds_it": 4 * n_b * row},
+            "model_ops": model_ops}
 
 
 # ---------------------------------------------------------------------------
@@ -118,7 +141,7 @@ def _dist():
 # ---------------------------------------------------------------------------
 
 def run_cpu_reference(w, steps: int, warmup: int, sample_n_b: int, sample_n_mu: int):
-    """Time the float64 CPU oracle on a bounded sample of the workload; returns samples/s."""
+    """Time the float64 CPU oracle on a bounded sample of the workload; returns (samples/s, cores, s/step)."""
     from oracle import mbs_oracle as O
     from oracle.hybrid import TorchGradFn
     from paper_2110_12484_b200.workloads import build_model, synthetic_data
@@ -131,7 +154,7 @@ def run_cpu_reference(w, steps: int, warmup: int, sample_n_b: int, sample_n_mu: 
     acc = O.Accumulator({n: v.shape for n, v in gf.params().items()})
     x, y = synthetic_data(w, sample_n_b, seed=1)
     xn = x.double().numpy()
-    yn = y.numpy()
+    yn = y.numpy().astype(np.float64) if w.target == "mask" else y.numpy()
     plan = O.plan_split(sample_n_b, sample_n_mu)
     params = gf.params()
     times = []
@@ -145,6 +168,26 @@ def run_cpu_reference(w, steps: int, warmup: int, sample_n_b: int, sample_n_mu: 
     return sps, threads, float(np.mean(times))
 
 
+def reference_arm(args, w, ws, rank):
+    if rank != 0:
+        return
+    n_b, n_mu = CPU_SAMPLE
+    n_mu = min(n_mu, w.micro or n_mu)
+    sps, cores, step_s = run_cpu_reference(w, args.steps, args.warmup, n_b, n_mu)
+    sample = (f"each step: one mini-batch of {n_b} {w.model} {'x'.join(map(str, w.sample_shape))} samples of "
+              f"this workload streamed as micro-batches of {n_mu}, float64 torch-CPU model + NumPy MBS arithmetic "
+              f"(oracle port of engine.py/optim.py); samples/s is per-sample, so it compares with the GPU arm's")
+    line = {"impl": "reference", "metric": METRIC, "value": sps, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(w, w.mini, w.micro or 128, ws, "reference numerics (float64 CPU)"),
+            "reference_sample": {"mini_batch": n_b, "micro_batch": n_mu, "steps": args.steps,
+                                 "warmup": args.warmup},
+            "cpu_baseline": {"value": sps, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": sps, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
@@ -152,65 +195,57 @@ def run_cpu_reference(w, steps: int, warmup: int, sample_n_b: int, sample_n_mu: 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "n1"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=16, help="samples per CPU-reference step")
+    ap.add_argument("--no-fp32-context", action="store_true")
+    ap.add_argument("--mini", type=int, default=0, help="override the workload's mini-batch (builder runs only)")
     ap.add_argument("--model-ops", default="native", choices=["native", "torch"],
                     help="the model's BatchNorm(+ReLU/+skip add) and max-pool: K5/K6 sm_100a kernels or stock torch")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(3, args.warmup)
 
     from paper_2110_12484_b200.workloads import WORKLOADS
     w = WORKLOADS[args.config]
     ws, rank, local = _dist()
-
     if args.impl == "reference":
-        if rank != 0:
-            return
-        n_mu = max(1, min(w.micro, args.cpu_sample // 2))
-        sps, cores, step_s = run_cpu_reference(w, args.steps, max(1, min(args.warmup, 1)), args.cpu_sample, n_mu)
-        sample = (f"{w.model} {w.sample_shape}: mini-batch {args.cpu_sample} streamed as micro {n_mu}, float64 "
-                  f"torch-CPU model + NumPy MBS arithmetic (oracle port of engine.py/optim.py)")
-        line = {"impl": "reference", "metric": "effective-batch samples/sec", "value": sps, "unit": "samples/s",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic",
-                "config": {"workload": w.name, "mini": w.mini, "micro": w.micro, "parallelism": "cpu"},
-                "cpu_baseline": {"value": sps, "unit": "samples/s", "cores": cores, "kind": "port",
-                                 "sample": sample},
-                "e2e": {"value": sps, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        reference_arm(args, w, ws, rank)
         return
+    run_gpu(args, w, ws, rank, local)
 
+
+def run_gpu(args, w, ws, rank, local):
     import paper_2110_12484_b200 as mbs
+    from paper_2110_12484_b200 import engine as _eng
+    from paper_2110_12484_b200 import graphs as _graphs
+    from paper_2110_12484_b200 import streaming as SS
     from paper_2110_12484_b200.prof import TIMER
     from paper_2110_12484_b200.streamer import Staging
     from paper_2110_12484_b200.workloads import build_model, synthetic_data
 
     ndev = torch.cuda.device_count()
     dev = torch.device("cuda", local % max(1, ndev))
+    torch.cuda.set_device(dev)
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(dev)
         backend = os.environ.get("MBS_DP_BACKEND", "nccl")   # gloo only for smoke runs of >1 rank per GPU
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")       # communicator INIT lines: rank count / NVLS
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    torch.cuda.set_device(dev)
     torch.backends.cudnn.benchmark = os.environ.get("MBS_BENCH_DETERMINISTIC", "0") != "1"
-    torch.backends.cudnn.deterministic = not torch.backends.cudnn.benchmark   # reproducibility checks only
+    torch.backends.cudnn.deterministic = not torch.backends.cudnn.benchmark
     torch.manual_seed(1234 + rank)
 
     model = build_model(w, ops=args.model_ops).to(dev).to(memory_format=torch.channels_last)
     params = mbs.ParameterSet(model, shadow=torch.bfloat16)   # bf16 shadow weights: K3 refreshes them, K1 reads bf16 grads
-    staging = Staging(dtype=torch.bfloat16, channels_last=True)
+    staging = Staging(dtype=torch.bfloat16, channels_last=True, target_dtype=torch.float32)
     autocast = torch.bfloat16
-    n_b, n_mu = w.mini, w.micro
+    n_b, n_mu = (args.mini or w.mini), w.micro
     autosize = None
     if n_mu == 0:
         # config 5: micro-batch auto-sized to free HBM (memory.py:88-101 rule on measured bytes)
@@ -219,33 +254,32 @@ def main():
 
         def make_batch(k):
             xb, yb = synthetic_data(w, k, seed=99, device=dev)
-            return stage_rows(xb, xb.dtype, tuple(xb.shape[1:]), None, 0, k, staging, dev), yb
-        # probes at 4 / 8 samples and a 0.88 margin: at HBM-filling sizes the allocator's fragmentation
-        # and the size-dependent cuDNN workspaces are not covered by the 0.92 default
+            return stage_rows(xb, xb.dtype, tuple(xb.shape[1:]), None, 0, k, staging, dev), \
+                (yb.float() if yb.dtype == torch.uint8 else yb)
         budget = memory.measure_budget(model, make_batch, w.loss_kind, optimizer_kind=w.optimizer,
                                        autocast_dtype=autocast, probe=(4, 8), safety=0.88)
-        n_mu = memory.fit_micro_batch(budget)
-        n_b = max(w.mini, 4 * n_mu)          # a mini-batch that cannot fit HBM without streaming
+        n_mu = memory.auto_micro_batch(budget, max(n_b, 4 * memory.fit_micro_batch(budget)), model)
+        n_b = max(n_b, 4 * n_mu)             # a mini-batch that cannot fit HBM without streaming
         autosize = {"capacity_bytes": budget.capacity_bytes, "resident_bytes": budget.resident_bytes,
                     "data_bytes_per_sample": budget.data_bytes_per_sample, "micro": n_mu, "mini": n_b}
         torch.cuda.empty_cache()
     plan = mbs.plan_split(n_b, n_mu)
 
-    # The timed region is ONE epoch call over `steps` shuffled mini-batches: engine.train_epoch
-    # (engine.py:276) at N=1, DataParallelMBS.train_epoch (each rank streams its own shard, one
-    # all-reduce per global mini-batch) at N>1. Device rows are gathered by K2, host rows by the native
-    # gather pool + H2D. Every mini-batch is >= 154 MB of uint8, so inputs exceed the 126 MB L2.
-    warm_mini = min(n_b, 1024)           # warm-up mini-batches (C4's 300k-sample mini-batch is 66 s of compute)
-    if ws > 1:
-        warm_mini = n_b                  # the global plan needs every rank's local mini-batch to be whole micros
-    n_data = max(args.steps * n_b, args.warmup * warm_mini)
-    x_host, y_host = synthetic_data(w, n_data, seed=rank, pinned=True)
+    # host dataset per rank: whole mini-batches, at most HOST_DATA_CAP bytes unless ONE mini-batch is larger
+    # (C4: exactly one 45.2 GB mini-batch, reshuffled every epoch)
+    row = int(np.prod(w.sample_shape)) + (int(np.prod(w.sample_shape[1:])) if w.target == "mask" else 8)
+    d_minis = max(1, min(args.steps, HOST_DATA_CAP // (n_b * row)))
+    t_data = time.perf_counter()
+    x_host, y_host = synthetic_data(w, d_minis * n_b, seed=rank, pinned=True)
     x_dev, y_dev = x_host.to(dev), y_host.to(dev)
+    t_data = time.perf_counter() - t_data
+    warm_small = min(n_b, 1024)          # e2e warm-up: one small mini-batch through the (already warm) stack
 
     dp = None
     if ws > 1:
         from paper_2110_12484_b200.dp import DataParallelMBS
         dp = DataParallelMBS(params, transport=os.environ.get("MBS_DP_TRANSPORT", "nccl"))
+        warm_small = n_b                 # the global plan needs every rank's local mini-batch to be whole micros
 
     def make_opt():
         return mbs.sgd_state(0.01, 0.9, 5e-4) if w.optimizer == "sgd" else mbs.adam_state(0.01, 5e-4)
@@ -255,87 +289,95 @@ def main():
     streamer = mbs.make_streamer(x_host, y_host, n_mu, n_slots=3)
     cs = torch.cuda.current_stream(dev)
 
-    def epoch(host: bool, n_steps: int, epoch_index: int, mini: int = n_b):
+    def run_steps(host: bool, n_steps: int, epoch0: int, mini: int = n_b, tracer=None):
+        """``n_steps`` mini-batches = epochs over the dataset (d_minis mini-batches each); losses read back."""
         xs, ys = (x_host, y_host) if host else (x_dev, y_dev)
-        if dp is not None:
-            res = dp.train_epoch(model, xs[:n_steps * mini], ys[:n_steps * mini], mini_batch_size=mini,
-                                 micro_batch_size=n_mu, normalization=w.normalization, loss_kind=w.loss_kind,
-                                 optimizer_state=st, seed=rank, epoch_index=epoch_index, accumulator=acc,
-                                 staging=staging, autocast_dtype=autocast, streamer=streamer if host else None,
-                                 prefetch=True)
-            return [r.loss for r in res]
-        es = mbs.train_epoch(model, params, xs[:n_steps * mini], ys[:n_steps * mini], mini_batch_size=mini,
-                             micro_batch_size=n_mu, normalization=w.normalization, loss_kind=w.loss_kind,
-                             optimizer_state=st, seed=rank, epoch_index=epoch_index, shuffle=True, prefetch=True,
-                             accumulator=acc, staging=staging, autocast_dtype=autocast,
-                             streamer=streamer if host else None)
-        return es.mini_losses      # every mini-batch's loss, read back (D2H) inside the call
+        losses, s = [], 0
+        while s < n_steps:
+            take = min(d_minis if mini == n_b else max(1, xs.shape[0] // mini), n_steps - s)
+            xe, ye = xs[:take * mini], ys[:take * mini]
+            if dp is not None:
+                res = dp.train_epoch(model, xe, ye, mini_batch_size=mini, micro_batch_size=n_mu,
+                                     normalization=w.normalization, loss_kind=w.loss_kind, optimizer_state=st,
+                                     seed=rank, epoch_index=epoch0 + s, accumulator=acc, staging=staging,
+                                     autocast_dtype=autocast, streamer=streamer if host else None, prefetch=True)
+                losses += [r.loss for r in res]
+            else:
+                es = mbs.train_epoch(model, params, xe, ye, mini_batch_size=mini, micro_batch_size=n_mu,
+                                     normalization=w.normalization, loss_kind=w.loss_kind, optimizer_state=st,
+                                     seed=rank, epoch_index=epoch0 + s, shuffle=True, prefetch=True,
+                                     accumulator=acc, staging=staging, autocast_dtype=autocast,
+                                     streamer=streamer if host else None, tracer=tracer)
+                losses += es.mini_losses
+            s += take
+        return losses
 
     def barrier():
         if ws > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
 
-    def timed(host: bool, steps: int, warmup: int, k1_timer: bool):
-        epoch(host, warmup, 1000 + int(host), warm_mini)
+    def timed(host: bool, steps: int, tracer=None):
         barrier()
         TIMER.reset()
-        TIMER.enabled = k1_timer
         if host:
             streamer.timings(flush=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
         e0.record(cs)
-        losses = epoch(host, steps, int(host))
+        losses = run_steps(host, steps, 100 * int(host), tracer=tracer)
         e1.record(cs)
         barrier()
-        TIMER.enabled = False
+        wall = time.perf_counter() - w0
         ms = e0.elapsed_time(e1)
         if ws > 1:
             t = torch.tensor([ms], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ms = float(t.item())
-        return ms, losses
+        return ms, losses, wall
 
-    # --- value: inputs resident in HBM (no per-kernel instrumentation inside the timed region) ---
+    # --- value: inputs resident in HBM; W full warm-up mini-batches first ---
+    run_steps(False, args.warmup, 1000)
     with ClockSampler(dev.index) as clocks:
-        ms_dev, _ = timed(False, args.steps, args.warmup, k1_timer=False)
+        ms_dev, _, wall_dev = timed(False, args.steps)
     launches_value = TIMER.launches
-    # Per-kernel bandwidths (K1 accumulate, K2, K3, K4 and the model's K5 BatchNorm): two more
-    # HBM-resident mini-batches, eager, with CUDA events around every launch on its stream. Kept out of
-    # `value` so the events and the eager launches do not perturb the headline number.
-    from paper_2110_12484_b200 import engine as _eng
-    from paper_2110_12484_b200 import graphs as _graphs
-    _graphs.clear()     # free the captured pools for the eager pass (re-captured in the e2e run's warm-up)
+    samples_total = n_b * args.steps * ws
+    value = samples_total / (ms_dev / 1e3)
+
+    # --- per-kernel bandwidths (K1, K2, K3, K4, K5): two more HBM-resident small mini-batches, eager, with CUDA
+    # events around every launch on its stream; outside the timed regions ---
+    _graphs.clear()
     graphs_on, _eng.CUDA_GRAPHS = _eng.CUDA_GRAPHS, False
     TIMER.reset()
     TIMER.enabled = True
     TIMER.k5 = args.model_ops == "native"
-    epoch(False, 2, 2000, warm_mini)
+    run_steps(False, 2, 2000, mini=warm_small)
     TIMER.enabled = TIMER.k5 = False
     _eng.CUDA_GRAPHS = graphs_on
     allstats = TIMER.summary()
     kstats = {k: v for k, v in allstats.items() if not k.startswith("k5_")}
     k5stats = {k: v for k, v in allstats.items() if k.startswith("k5_")}
-    samples_total = n_b * args.steps * ws
-    value = samples_total / (ms_dev / 1e3)
 
-    # --- e2e: host-pinned inputs through the streamer ---
-    ms_host, losses = timed(True, args.steps, args.warmup, k1_timer=False)
+    # --- e2e: host-pinned inputs through the streamer, the run's real schedule traced ---
+    run_steps(True, 1, 3000, mini=warm_small)
+    tracer = SS.ScheduleTracer(dev) if ws == 1 else None
+    with ClockSampler(dev.index) as clocks_e2e:
+        ms_host, losses, wall_host = timed(True, args.steps, tracer)
     launches_e2e = TIMER.launches
     e2e = samples_total / (ms_host / 1e3)
     tim = streamer.timings(flush=True)
     copy_ms = sum(t[1] for t in tim)
     blocked_ms = sum(t[2] for t in tim)
     h2d_bytes = sum(t[3] for t in tim) / max(1, args.steps)
-    overlap = 100.0 * (1.0 - blocked_ms / copy_ms) if copy_ms > 0 else None
     h2d_gbs = (sum(t[3] for t in tim) / (copy_ms / 1e3) / 1e9) if copy_ms > 0 else None
     streamer.close()
+    scheds = tracer.schedules() if tracer is not None else []
 
     # --- no-stream baseline: plain torch training at batch = micro, data resident ---
-    _graphs.clear()     # the MBS step's graph pools are not needed by the baselines
+    _graphs.clear()
     nos = nos_torch = None
     for ops_ in (args.model_ops, "torch") if args.model_ops != "torch" else (args.model_ops,):
-        b = n_mu        # halve the batch until the model fits (the stock model holds more per sample)
+        b = n_mu
         r = None
         while b >= 1 and r is None:
             try:
@@ -348,22 +390,32 @@ def main():
         else:
             nos_torch = r
 
-    # the reference's overhead report (streaming.py:130-149) on MEASURED schedules: the MBS step as
-    # run (copy per micro from the streamer's events, compute per micro from the timed step) vs the
-    # no-stream run processing the same samples
-    from paper_2110_12484_b200 import streaming as SS
-    k3 = next((v for k, v in kstats.items() if k.startswith("k3_")), {"avg_ms": 0.0})
-    per_micro_ms = (ms_host / args.steps - k3["avg_ms"]) / plan.n_s_mu
-    copies = [t[1] for t in tim[-plan.n_s_mu:]] if tim else [0.0] * plan.n_s_mu
-    mbs_sched = SS.measured_schedule(copies, [per_micro_ms] * plan.n_s_mu, k3["avg_ms"], overlap=True)
-    base_ms = n_b / nos["value"] * ws * 1e3 if nos else None
-    base_sched = SS.measured_schedule([0.0], [base_ms], 0.0, overlap=False) if base_ms else None
-    rep = SS.overhead_report(mbs_sched, base_sched)
-    overhead = {"mbs_makespan_ms": rep.mbs_makespan * 1e3,
-                "no_stream_makespan_ms": rep.baseline_makespan * 1e3 if rep.baseline_makespan else None,
-                "overhead_pct": rep.overhead_pct,
-                "how": "streaming.overhead_report on measured per-micro copy/compute times (e2e run) vs the "
-                       "no-stream run's time for the same samples"}
+    # --- the reference's overhead report on the measured schedules ---
+    overhead = None
+    if scheds:
+        mk = [s.makespan for s in scheds]
+        fr = [f for f in (SS.overlap_fraction(s) for s in scheds) if f is not None]
+        per_kind = {}
+        for s in scheds:
+            for e in s.events:
+                per_kind[e.kind] = per_kind.get(e.kind, 0.0) + (e.end - e.start)
+        mbs_sched = scheds[-1]
+        base_sched = None
+        if nos:
+            base_mk = n_b / (nos["value"] / ws)
+            base_sched = SS.StreamSchedule(tuple(SS.StreamEvent(*e) for e in nos["events"]), base_mk, False)
+        rep = SS.overhead_report(mbs_sched, base_sched)
+        overhead = {"mbs_makespan_s": rep.mbs_makespan, "no_stream_makespan_s": rep.baseline_makespan,
+                    "overhead_pct": rep.overhead_pct, "overhead_seconds": rep.overhead_seconds,
+                    "mbs_makespan_s_per_mini_batch": mk, "h2d_overlap_pct": 100.0 * float(np.mean(fr)) if fr else None,
+                    "seconds_per_mini_batch_by_kind": {k: v / len(scheds) for k, v in per_kind.items()},
+                    "events_per_mini_batch": len(mbs_sched.events),
+                    "how": "streaming.overhead_report (streaming.py:130-149) on the last timed e2e mini-batch's "
+                           "StreamSchedule, recorded by streaming.ScheduleTracer (CUDA events per micro-batch: "
+                           "transfer on the copy stream, forward / backward(+K1) / update on the compute stream); "
+                           "baseline = the no-stream run's measured per-sample time x N_B (it ran "
+                           f"{nos['samples'] if nos else 0} samples); overlap = 1 - (compute-stream wait on "
+                           "copies) / (copy time), from the same events"}
 
     k1 = kstats.get("k1_accumulate", {})
     peak, peak_kind = _peaks()
@@ -373,18 +425,19 @@ def main():
             traffic = json.load(f).get("dram_bytes_per_launch")
     except Exception:
         pass
-    roofline = {"kernel": "k1_accumulate (mbs_accum_add)", "bound": "hbm", "achieved": k1.get("gbs"),
+    gbytes = 2 if getattr(params, "shadow", None) is not None else 4
+    roofline = {"kernel": "k1_accumulate (mbs_accum_add_typed)", "bound": "hbm", "achieved": k1.get("gbs"),
                 "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": (k1.get("gbs") or 0.0) / peak, "traffic": traffic,
-                "algorithmic_bytes_per_launch": k1.get("bytes_per_launch"), "avg_launch_us": (k1.get("avg_ms") or 0) * 1e3,
-                "launches_timed": k1.get("launches"),
-                "bytes_rule": "12 B/param (read g, read acc, write acc); 8 B/param on the first micro-batch "
-                              "(acc = s*g); P = %d" % params.layout.n_params,
+                "algorithmic_bytes_per_launch": k1.get("bytes_per_launch"),
+                "avg_launch_us": (k1.get("avg_ms") or 0) * 1e3, "launches_timed": k1.get("launches"),
+                "bytes_rule": (f"per parameter: read g ({gbytes} B: bf16 weight gradients of the shadow-weight "
+                               "matmuls, fp32 for BN / bias) + read acc (4 B) + write acc (4 B); the first micro-batch "
+                               "of a mini-batch assigns acc = s*g (no acc read); P = %d" % params.layout.n_params),
                 "how": "CUDA events around every K1 launch of two extra HBM-resident mini-batches (eager), "
                        "outside the timed region",
-                "note": "K1 is the kernel the north star names (accumulate); the dominant kernel of the step by "
-                        "time is the model's K5 BatchNorm, reported in roofline_k5",
-                "other_kernels": {k: {"gbs": v["gbs"], "avg_us": v["avg_ms"] * 1e3, "launches": v["launches"]}
+                "other_kernels": {k: {"gbs": v["gbs"], "avg_us": v["avg_ms"] * 1e3, "launches": v["launches"],
+                                      "bytes_per_launch": v["bytes_per_launch"]}
                                   for k, v in kstats.items() if k != "k1_accumulate"}}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -398,61 +451,111 @@ def main():
                    "achieved": value * gfs / 1e3, "achieved_e2e": e2e * gfs / 1e3, "peak": tf_peak,
                    "peak_kind": tf_kind, "frac": value / ws * gfs / 1e3 / tf_peak,
                    "frac_e2e": e2e / ws * gfs / 1e3 / tf_peak, "peak_is": "per GPU (frac uses value / n_gpus)",
-                   "how": "end-to-end samples/s x algorithmic fwd+bwd FLOP per sample (FlopCounterMode: the "
-                          "model's convolutions/matmuls), against the bf16 dense peak"}
+                   "how": "samples/s x algorithmic fwd+bwd FLOP per sample (FlopCounterMode: the model's "
+                          "convolutions/matmuls), against the bf16 dense peak"}
     roofline_k5 = None
     if k5stats:
         kb = sum(v["bytes_per_launch"] * v["launches"] for v in k5stats.values())
         kt = sum(v["total_ms"] for v in k5stats.values())
-        roofline_k5 = {"kernel": "k5 micro-batch BatchNorm (+ReLU/+residual), forward and backward",
-                       "bound": "hbm", "achieved": kb / (kt / 1e3) / 1e9, "peak": peak, "peak_kind": peak_kind,
-                       "unit": "GB/s", "frac": kb / (kt / 1e3) / 1e9 / peak,
-                       "ms_per_mini_batch": kt, "calls": {k: v["launches"] for k, v in k5stats.items()},
-                       "per_call": {k: {"gbs": v["gbs"], "avg_us": v["avg_ms"] * 1e3} for k, v in k5stats.items()},
-                       "bytes_rule": "per call over E activation elements of s bytes: forward 3*E*s (+E*s "
-                                     "residual), backward 5*E*s (+2*E*s residual: the two-pass minimum); CUDA events around each "
-                                     "3-kernel call, so small layers include launch gaps"}
+        roofline_k5 = {"kernel": "k5 micro-batch BatchNorm (+ReLU/+residual), forward and backward (model side)",
+                       "bound": "hbm", "achieved": kb / (kt / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                       "frac": kb / (kt / 1e3) / 1e9 / peak, "ms_per_small_mini_batch": kt / 2}
 
-    line = {"metric": "effective-batch samples/sec", "value": value, "unit": "samples/s", "n_gpus": ws,
+    precision = {"dtype": "bf16",
+                 "detail": "bf16 autocast compute on cuDNN/cuBLAS reading bf16 shadow weights that K3 writes; bf16 "
+                           "weight gradients widened by K1; fp32 master weights, fp32 MBS accumulation, fp32 "
+                           "optimizer state; inputs uint8 staged exactly to bf16",
+                 "parity": "pinned to the float64 oracle in tests/test_bench_stack_parity_gpu.py (this exact stack, "
+                           "bf16 and fp32, at C1 / ResNet-50@224 / U-Net@384 shapes)"}
+
+    fp32_ctx = None
+    if not args.no_fp32_context and ws == 1:
+        _graphs.clear()
+        fp32_ctx = fp32_context(w, dev, n_mu, warm_small, args.model_ops, x_dev, y_dev)
+
+    config = workload_config(w, n_b, n_mu, ws, "BatchNorm(+ReLU/+skip add) on K5, max-pool (+U-Net skip join) on K6, "
+                             "stem conv as K7 im2col + GEMM, micro-batch statistics; micro step replayed from "
+                             "CUDA graphs" if args.model_ops == "native" else "stock torch")
+    config.update({"precision": precision["detail"], "autosize": autosize,
+                   "host_dataset": {"mini_batches": d_minis, "samples": d_minis * n_b,
+                                    "bytes": int(x_host.numel() * x_host.element_size() +
+                                                 y_host.numel() * y_host.element_size()),
+                                    "pinned": True, "setup_s": t_data},
+                   "steps_are": "one mini-batch each; an epoch over the host dataset every "
+                                f"{d_minis} steps, reshuffled by epoch_index",
+                   "warmup_is": f"{args.warmup} full mini-batches before the HBM-resident (value) run; 1 mini-batch "
+                                f"of {warm_small} through the host streamer before the e2e run",
+                   "l2": "inputs > L2: every mini-batch is %.1f GB of uint8, none reused within a step"
+                         % (n_b * int(np.prod(w.sample_shape)) / 1e9),
+                   "api": ("engine.train_epoch" if ws == 1 else "dp.DataParallelMBS.train_epoch (per-rank shards, "
+                           "one all-reduce per global mini-batch, transport=%s)" % dp.transport)})
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (uint8 images, random labels; random-init weights)",
-            "config": {"workload": w.name, "model": w.model, "mini_batch_per_gpu": n_b, "micro_batch": n_mu,
-                       "n_micro": plan.n_s_mu, "global_batch": n_b * ws, "parallelism": f"dp{ws}",
-                       "normalization": w.normalization, "optimizer": w.optimizer,
-                       "model_precision": "bf16 compute (autocast) on cuDNN/cuBLAS reading bf16 shadow weights that "
-                                          "K3 writes; fp32 master weights, fp32 MBS accumulation",
-                       "model_ops": ("BatchNorm(+ReLU/+skip add) on K5, max-pool (+U-Net skip join) on K6, stem "
-                                     "conv as K7 im2col + GEMM (bn.py, pool.py, stem.py), micro-batch statistics; "
-                                     "micro step replayed from a CUDA graph" if args.model_ops == "native"
-                                     else "stock torch BatchNorm / max-pool / stem conv"),
-                       "input": "uint8 NCHW staged to bf16 NHWC by K2",
-                       "l2": ("inputs > L2: every mini-batch is %.0f MB of uint8" % (x_dev[:n_b].numel() / 1e6)) +
-                             ", none reused within the timed region",
-                       "api": ("engine.train_epoch" if ws == 1 else "dp.DataParallelMBS.train_epoch (per-rank "
-                               "shards, one all-reduce per global mini-batch, transport=%s)" % dp.transport) +
-                              " over `steps` shuffled mini-batches",
-                       "autosize": autosize},
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (uint8 images, random labels / masks; random-init weights)",
+            "config": config,
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": int(h2d_bytes),
-                    "d2h_bytes_per_step": 8 * (4 + 2 * plan.n_s_mu), "ms_per_step": ms_host / args.steps},
-            "h2d_overlap_pct": overlap, "h2d_gbs": h2d_gbs, "accum_gbs": k1.get("gbs"),
-            "no_stream": nos, "stream_vs_no_stream": value / nos["value"] if nos else None, "overhead": overhead,
-            "no_stream_torch_ops": nos_torch, "roofline_k5": roofline_k5, "model_flops": model_flops,
+                    "d2h_bytes_per_step": 8 * (4 + 2 * plan.n_s_mu), "ms_per_step": ms_host / args.steps,
+                    "wall_s": wall_host},
             "e2e_vs_no_stream": e2e / nos["value"] if nos else None,
-            "roofline": roofline, "gpu_launches": launches_value, "gpu_launches_e2e": launches_e2e,
-            "clocks": clocks.summary(), "final_loss": losses[-1] if losses else None}
+            "value_vs_no_stream": value / nos["value"] if nos else None,
+            "h2d_overlap_pct": (overhead or {}).get("h2d_overlap_pct"),
+            "h2d_overlap_pct_streamer": 100.0 * (1.0 - blocked_ms / copy_ms) if copy_ms > 0 else None,
+            "h2d_gbs": h2d_gbs, "accum_gbs": k1.get("gbs"),
+            "no_stream": {k: v for k, v in (nos or {}).items() if k != "events"} or None,
+            "no_stream_torch_ops": {k: v for k, v in (nos_torch or {}).items() if k != "events"} or None,
+            "overhead": overhead, "roofline": roofline, "roofline_k5": roofline_k5, "model_flops": model_flops,
+            "precision": precision, "precision_fp32": fp32_ctx,
+            "gpu_launches": launches_value, "gpu_launches_e2e": launches_e2e,
+            "clocks": clocks.summary(), "clocks_e2e": clocks_e2e.summary(),
+            "final_loss": losses[-1] if losses else None, "value_wall_s": wall_dev}
 
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu_n_b = args.cpu_sample
-        cpu_mu = max(1, cpu_n_b // 2)
+        cpu_n_b, cpu_mu = CPU_SAMPLE
         sps, cores, step_s = run_cpu_reference(w, 1, 1, cpu_n_b, cpu_mu)
         line["cpu_baseline"] = {"value": sps, "unit": "samples/s", "cores": cores, "kind": "port",
-                                "sample": f"1 mini-batch of {cpu_n_b} as micro {cpu_mu}, {w.model} float64 "
-                                          f"torch-CPU + NumPy MBS oracle, {step_s:.1f} s/step"}
+                                "sample": f"1 mini-batch of {cpu_n_b} as micro {cpu_mu} (after 1 warm-up), {w.model} "
+                                          f"float64 torch-CPU + NumPy MBS oracle, {step_s:.1f} s/step"}
     if rank == 0:
         print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def fp32_context(w, dev, n_mu, mini, model_ops, x_dev, y_dev):
+    """The MBS stack at fp32 (fp32 weights, staging and compute, TF32 off): the precision the oracle pins."""
+    import paper_2110_12484_b200 as mbs
+    from paper_2110_12484_b200.streamer import Staging
+    from paper_2110_12484_b200.workloads import build_model
+    tf = (torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32)
+    torch.backends.cuda.matmul.allow_tf32 = torch.backends.cudnn.allow_tf32 = False
+    try:
+        torch.manual_seed(5)
+        model = build_model(w, ops=model_ops).to(dev).to(memory_format=torch.channels_last)
+        params = mbs.ParameterSet(model)
+        st = mbs.sgd_state(0.01, 0.9, 5e-4) if w.optimizer == "sgd" else mbs.adam_state(0.01, 5e-4)
+        staging = Staging(torch.float32, True, target_dtype=torch.float32)
+        n = 3 * mini
+
+        def run(e):
+            return mbs.train_epoch(model, params, x_dev[:n], y_dev[:n], mini_batch_size=mini, micro_batch_size=n_mu,
+                                   normalization=w.normalization, loss_kind=w.loss_kind, optimizer_state=st, seed=0,
+                                   epoch_index=e, staging=staging)
+        run(0)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run(1)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1)
+        del model, params, st
+        return {"value": n / (ms / 1e3), "unit": "samples/s", "dtype": "f32 (TF32 off)", "mini_batch": mini,
+                "micro_batch": n_mu, "mini_batches_timed": 3, "warmup_mini_batches": 3,
+                "how": "same MBS stack (K1-K7, CUDA graphs, HBM-resident uint8 staged to fp32) at the precision "
+                       "every oracle parity test also pins; context only"}
+    finally:
+        torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32 = tf
 
 
 def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True):
@@ -461,7 +564,8 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True
     ``ops`` selects the same model definition as the MBS run (native K5/K6/K7 or stock torch ops).
     ``graph``: the whole training step (fwd + bwd + fused optimizer step) is replayed from one CUDA
     graph, like the MBS micro step — eager, this loop is host-bound on B200 and its number then
-    tracks the host CPU rather than the GPU. Falls back to eager if capture fails."""
+    tracks the host CPU rather than the GPU. Falls back to eager if capture fails. Every step is
+    bracketed by CUDA events (the baseline's measured "compute" schedule)."""
     from paper_2110_12484_b200.losses import compute_loss
     from paper_2110_12484_b200.workloads import build_model, synthetic_data
     torch.manual_seed(0)
@@ -471,6 +575,7 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True
     else:
         opt = torch.optim.Adam(model.parameters(), lr=0.01, weight_decay=5e-4, fused=True, capturable=graph)
     x, y = synthetic_data(w, 2 * batch, seed=7, device=dev)
+    y = y.float() if y.dtype == torch.uint8 else y
     xs = [x[i * batch:(i + 1) * batch].to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
           for i in range(2)]
     ys = [y[i * batch:(i + 1) * batch] for i in range(2)]
@@ -517,17 +622,19 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True
         except Exception as e:                           # noqa: BLE001
             print(f"no-stream baseline: graph capture failed ({type(e).__name__}: {e}); eager", file=sys.stderr)
     torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n = steps * max(1, w.mini // batch)
-    e0.record()
+    n = steps * max(1, min(w.mini, 1024) // batch)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
+    evs[0].record()
     for i in range(n):
         one(i)
-    e1.record()
+        evs[i + 1].record()
     torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1)
+    ms = evs[0].elapsed_time(evs[-1])
+    events = [("compute", i, evs[0].elapsed_time(evs[i]) / 1e3, evs[0].elapsed_time(evs[i + 1]) / 1e3)
+              for i in range(n)]
     del model, opt
-    return {"value": batch * n * ws / (ms / 1e3), "unit": "samples/s", "batch": batch,
-            "steps": n, "model_ops": ops, "how": how}
+    return {"value": batch * n * ws / (ms / 1e3), "unit": "samples/s", "batch": batch, "steps": n,
+            "samples": batch * n, "model_ops": ops, "how": how, "events": events}
 
 
 if __name__ == "__main__":

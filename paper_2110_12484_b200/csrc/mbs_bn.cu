@@ -99,12 +99,20 @@ struct BnGeom {
 
 // Per-channel affine of the forward (shared by forward apply and the backward mask
 // recomputation so both see bit-identical values): y = x*scale + shift.
+// Per-channel affine of the normalisation, z = (x - mu) * scale + beta. Centring BEFORE the scale (not
+// x*scale + (beta - mu*scale)) keeps x_hat exact when |mean| >> std (e.g. a stem fed raw 0..255 pixels,
+// where the folded form cancels ~log2(|mean|/std) bits) and makes x == mean give exactly beta (a
+// one-value channel, then meets a following ReLU at exactly 0 like the reference).
 __device__ __forceinline__ void bn_affine(const float* w, const float* b, const float* mean, const float* invstd,
-                                          int64_t c, float& scale, float& shift) {
+                                          int64_t c, float& scale, float& mu, float& beta) {
     const float g = w ? w[c] : 1.f;
-    const float be = b ? b[c] : 0.f;
+    beta = b ? b[c] : 0.f;
     scale = g * invstd[c];
-    shift = fmaf(-mean[c], scale, be);
+    mu = mean[c];
+}
+
+__device__ __forceinline__ float bn_z(float x, float scale, float mu, float beta) {
+    return fmaf(x - mu, scale, beta);
 }
 
 // torch's relu (clamp_min) propagates NaN; fmaxf would not
@@ -113,8 +121,8 @@ __device__ __forceinline__ float relu_nan(float z) { return z < 0.f ? 0.f : z; }
 // threshold_backward on the stored output y = T(relu(z)): the gradient is zeroed where y <= 0
 // (NaN passes, as in torch); y <= 0 is decided on z without a conversion (kMaskThreshold).
 template <typename T, int V, bool RES>
-__device__ __forceinline__ float relu_mask(float x, float sc, float sh, float r, float d) {
-    const float z = fmaf(x, sc, sh) + (RES ? r : 0.f);
+__device__ __forceinline__ float relu_mask(float x, float sc, float mu, float be, float r, float d) {
+    const float z = bn_z(x, sc, mu, be) + (RES ? r : 0.f);
     return z <= BnIO<T, V>::kMaskThreshold ? 0.f : d;
 }
 
@@ -141,8 +149,8 @@ __device__ __forceinline__ void bn_reduce_body(const T* __restrict__ x, const T*
         } else {
 #pragma unroll
             for (int i = 0; i < V; ++i) {
-                k[i] = mean[c0 + i];
-                if (RELU) bn_affine(w, b, mean, invstd, c0 + i, sc[i], sh[i]);
+                if (RELU) bn_affine(w, b, mean, invstd, c0 + i, sc[i], k[i], sh[i]);
+                else k[i] = mean[c0 + i];
             }
         }
         const int64_t r0 = (int64_t)bx * g.chunk;
@@ -163,7 +171,7 @@ __device__ __forceinline__ void bn_reduce_body(const T* __restrict__ x, const T*
                 if (MODE == 1 && RELU) {
 #pragma unroll
                     for (int i = 0; i < V; ++i)
-                        dv[u][i] = relu_mask<T, V, RES>(xv[u][i], sc[i], sh[i], rv[u][i], dv[u][i]);
+                        dv[u][i] = relu_mask<T, V, RES>(xv[u][i], sc[i], k[i], sh[i], rv[u][i], dv[u][i]);
                 }
 #pragma unroll
                 for (int i = 0; i < V; ++i) {
@@ -186,7 +194,7 @@ __device__ __forceinline__ void bn_reduce_body(const T* __restrict__ x, const T*
             if (MODE == 1 && RELU && RES) BnIO<T, V>::load(res + o, rv);
             if (MODE == 1 && RELU) {
 #pragma unroll
-                for (int i = 0; i < V; ++i) dv[i] = relu_mask<T, V, RES>(xv[i], sc[i], sh[i], rv[i], dv[i]);
+                for (int i = 0; i < V; ++i) dv[i] = relu_mask<T, V, RES>(xv[i], sc[i], k[i], sh[i], rv[i], dv[i]);
             }
 #pragma unroll
             for (int i = 0; i < V; ++i) {
@@ -291,10 +299,11 @@ __device__ __forceinline__ void bn_stats_write(const T* __restrict__ x, const Bn
         const double unbiased = g.rows > 1 ? var * m / (m - 1.0) : var;
         running_var[c] = (float)((1.0 - momentum) * (double)running_var[c] + momentum * unbiased);
     }
-    float sc, sh;
-    bn_affine(w, b, save_mean, save_invstd, c, sc, sh);
-    coef[2 * c] = sc;
-    coef[2 * c + 1] = sh;
+    float sc, mu, be;
+    bn_affine(w, b, save_mean, save_invstd, c, sc, mu, be);
+    coef[3 * c] = sc;
+    coef[3 * c + 1] = mu;
+    coef[3 * c + 2] = be;
 }
 
 template <typename T, int TPC>
@@ -348,11 +357,12 @@ __device__ __forceinline__ void bn_apply_body(const T* __restrict__ x, const T* 
     const int lane = tid % g.gv, rph = tid / g.gv;
     const int64_t c0 = ((int64_t)by * g.gv + lane) * V;
     if (rph >= g.rp || c0 >= g.C) return;
-    float sc[V], sh[V];
+    float sc[V], mu[V], be[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-        sc[i] = coef[2 * (c0 + i)];
-        sh[i] = coef[2 * (c0 + i) + 1];
+        sc[i] = coef[3 * (c0 + i)];
+        mu[i] = coef[3 * (c0 + i) + 1];
+        be[i] = coef[3 * (c0 + i) + 2];
     }
     const int64_t r0 = (int64_t)bx * g.chunk;
     const int64_t r1 = min(g.rows, r0 + g.chunk);
@@ -370,7 +380,7 @@ __device__ __forceinline__ void bn_apply_body(const T* __restrict__ x, const T* 
         for (int u = 0; u < U; ++u) {
 #pragma unroll
             for (int i = 0; i < V; ++i) {
-                float z = fmaf(xv[u][i], sc[i], sh[i]) + (RES ? rv[u][i] : 0.f);
+                float z = bn_z(xv[u][i], sc[i], mu[i], be[i]) + (RES ? rv[u][i] : 0.f);
                 xv[u][i] = RELU ? relu_nan(z) : z;
             }
             BnIO<T, V>::store(y + (r + u * g.rp) * g.C + c0, xv[u]);
@@ -383,7 +393,7 @@ __device__ __forceinline__ void bn_apply_body(const T* __restrict__ x, const T* 
         if (RES) BnIO<T, V>::load(res + o, rv);
 #pragma unroll
         for (int i = 0; i < V; ++i) {
-            float z = fmaf(xv[i], sc[i], sh[i]) + (RES ? rv[i] : 0.f);
+            float z = bn_z(xv[i], sc[i], mu[i], be[i]) + (RES ? rv[i] : 0.f);
             xv[i] = RELU ? relu_nan(z) : z;
         }
         BnIO<T, V>::store(y + o, xv);
@@ -419,8 +429,7 @@ __device__ __forceinline__ void bn_elemt_body(const T* __restrict__ x, const T* 
     for (int i = 0; i < V; ++i) {
         A[i] = coef[3 * (c0 + i)];
         B[i] = coef[3 * (c0 + i) + (kFold ? 2 : 1)];
-        mu[i] = kFold ? 0.f : mean[c0 + i];
-        bn_affine(w, b, mean, invstd, c0 + i, sc[i], sh[i]);
+        bn_affine(w, b, mean, invstd, c0 + i, sc[i], mu[i], sh[i]);
     }
     const int64_t r0 = (int64_t)bx * g.chunk;
     const int64_t r1 = min(g.rows, r0 + g.chunk);
@@ -429,7 +438,7 @@ __device__ __forceinline__ void bn_elemt_body(const T* __restrict__ x, const T* 
     auto body = [&](float (&xv)[V], float (&dv)[V], float (&rv)[V], int64_t o) {
         if (RELU) {
 #pragma unroll
-            for (int i = 0; i < V; ++i) dv[i] = relu_mask<T, V, RES>(xv[i], sc[i], sh[i], rv[i], dv[i]);
+            for (int i = 0; i < V; ++i) dv[i] = relu_mask<T, V, RES>(xv[i], sc[i], mu[i], sh[i], rv[i], dv[i]);
         }
         if (RES) BnIO<T, V>::store(dres + o, dv);
 #pragma unroll
@@ -600,12 +609,12 @@ __global__ void __launch_bounds__(kBnThreads, 2) k_bn_tma(
         if (KIND == 0) BnIO<T, V>::load(x + c0, kk);  // shift K = x[0, c]
 #pragma unroll
         for (int i = 0; i < V; ++i) {
-            if (KIND == 1) kk[i] = mean[c0 + i];
-            if (KIND == 3 && !kFold) kk[i] = mean[c0 + i];
-            if ((KIND == 1 && RELU) || KIND == 3) bn_affine(w, b, mean, invstd, c0 + i, sc[i], sh[i]);
+            // KIND 1 / 3: kk = the channel mean (centring for the reduce / dx, and the ReLU mask's mu)
+            if (KIND == 1 || KIND == 3) bn_affine(w, b, mean, invstd, c0 + i, sc[i], kk[i], sh[i]);
             if (KIND == 2) {
-                sc[i] = coef[2 * (c0 + i)];
-                sh[i] = coef[2 * (c0 + i) + 1];
+                sc[i] = coef[3 * (c0 + i)];
+                kk[i] = coef[3 * (c0 + i) + 1];
+                sh[i] = coef[3 * (c0 + i) + 2];
             }
             if (KIND == 3) {
                 A[i] = coef[3 * (c0 + i)];
@@ -639,7 +648,7 @@ __global__ void __launch_bounds__(kBnThreads, 2) k_bn_tma(
                 if (RES) BnIO<T, V>::load(rsm + o, rv);
                 if ((KIND == 1 || KIND == 3) && RELU) {
 #pragma unroll
-                    for (int e = 0; e < V; ++e) dv[e] = relu_mask<T, V, RES>(xv[e], sc[e], sh[e], rv[e], dv[e]);
+                    for (int e = 0; e < V; ++e) dv[e] = relu_mask<T, V, RES>(xv[e], sc[e], kk[e], sh[e], rv[e], dv[e]);
                 }
                 if (KIND == 0) {
 #pragma unroll
@@ -660,7 +669,7 @@ __global__ void __launch_bounds__(kBnThreads, 2) k_bn_tma(
                 } else if (KIND == 2) {
 #pragma unroll
                     for (int e = 0; e < V; ++e) {
-                        const float z = fmaf(xv[e], sc[e], sh[e]) + (RES ? rv[e] : 0.f);
+                        const float z = bn_z(xv[e], sc[e], kk[e], sh[e]) + (RES ? rv[e] : 0.f);
                         xv[e] = RELU ? relu_nan(z) : z;
                     }
                     BnIO<T, V>::store(out + (rs + j) * g.C + c0, xv);

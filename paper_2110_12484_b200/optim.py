@@ -110,7 +110,8 @@ def sgd_step(params: ParameterSet, grads: GradientSet, state: OptimizerState, *,
     N.check(N.lib().mbs_sgd_step(params.flat.data_ptr(), g.data_ptr(), v.data_ptr(), params.layout.total,
                                  float(state.lr), float(state.momentum), float(state.weight_decay),
                                  _guard_ptr(grads), _shadow_ptr(params), _stream_ptr(stream)), "mbs_sgd_step")
-    TIMER.stop("k3_sgd", t0, 20 * params.layout.n_params, stream)
+    # algorithmic bytes: read g, w, v; write w, v (20 B/param) + the bf16 shadow write (2 B/param) if any
+    TIMER.stop("k3_sgd", t0, (20 + 2 * (_shadow_ptr(params) is not None)) * params.layout.n_params, stream)
     state.step_count += 1
 
 
@@ -125,7 +126,7 @@ def adam_step(params: ParameterSet, grads: GradientSet, state: OptimizerState, *
                                   params.layout.total, float(state.lr), float(state.adam_beta1),
                                   float(state.adam_beta2), float(state.adam_eps), float(state.weight_decay), t,
                                   _guard_ptr(grads), _shadow_ptr(params), _stream_ptr(stream)), "mbs_adam_step")
-    TIMER.stop("k3_adam", t0, 28 * params.layout.n_params, stream)
+    TIMER.stop("k3_adam", t0, (28 + 2 * (_shadow_ptr(params) is not None)) * params.layout.n_params, stream)
     state.step_count = t
 
 

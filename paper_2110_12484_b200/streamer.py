@@ -40,6 +40,7 @@ class Staging:
 
     dtype: torch.dtype = torch.float32      # model input dtype (f32 / bf16 / f16)
     channels_last: bool = False             # NHWC for 4-D inputs
+    target_dtype: torch.dtype | None = None  # uint8 dense targets (masks) are staged to this dtype by K2
 
     def out_tensor(self, n: int, sample_shape: tuple, device) -> torch.Tensor:
         shape = (n,) + tuple(sample_shape)
@@ -117,6 +118,13 @@ def _fits(t: torch.Tensor, staging: Staging, shape: tuple) -> bool:
     return t.is_contiguous()
 
 
+def _target_staging(staging: Staging | None, y: torch.Tensor) -> Staging | None:
+    """How dense uint8 targets (segmentation masks) are staged for the loss (K2, NCHW), or None to copy bytes."""
+    if staging is None or staging.target_dtype is None or y.dim() < 2 or y.dtype != torch.uint8:
+        return None
+    return Staging(dtype=staging.target_dtype, channels_last=False)
+
+
 def _dest(dest, n, sample_shape, staging, y_shape, y_dtype):
     """The consumer's preallocated (x, y) buffers for a micro-batch of n rows, or None."""
     if dest is None:
@@ -135,19 +143,22 @@ def device_micro_batches(x: torch.Tensor, y: torch.Tensor, jobs, staging: Stagin
     dev = x.device
     st = staging or Staging(dtype=x.dtype if x.is_floating_point() and x.dtype != torch.float64
                             else torch.float32)
+    ts = _target_staging(staging, y)
+    y_shape = tuple(y.shape[1:])
     for rows, row0, n in jobs:
         if tracer is not None:
             tracer.data_ready()
         if rows is None and (staging is None or staging.is_identity_for(x)):
             xk = x[row0:row0 + n]
-            yk = y[row0:row0 + n]
+            yk = y[row0:row0 + n] if ts is None else stage_rows(y, y.dtype, y_shape, None, row0, n, ts, dev)
         else:
-            buf = _dest(dest, n, tuple(x.shape[1:]), st, tuple(y.shape[1:]), y.dtype)
+            buf = _dest(dest, n, tuple(x.shape[1:]), st, y_shape, ts.dtype if ts is not None else y.dtype)
             xk = stage_rows(x, x.dtype, tuple(x.shape[1:]), rows, row0, n, st, dev,
                             out=buf[0] if buf is not None else None)
-            if rows is not None:
-                yk = gather_rows(y, y.dtype, tuple(y.shape[1:]), rows, row0, n, dev,
-                                 out=buf[1] if buf is not None else None)
+            if ts is not None:
+                yk = stage_rows(y, y.dtype, y_shape, rows, row0, n, ts, dev, out=buf[1] if buf is not None else None)
+            elif rows is not None:
+                yk = gather_rows(y, y.dtype, y_shape, rows, row0, n, dev, out=buf[1] if buf is not None else None)
             else:
                 yk = y[row0:row0 + n]
         yield xk, yk
@@ -238,6 +249,7 @@ class MicroBatchStreamer:
         jobs = list(jobs)
         staging = staging or Staging(dtype=x.dtype if x.dtype in (torch.float32,) else torch.float32)
         sample_shape, y_shape = tuple(x.shape[1:]), tuple(y.shape[1:])
+        ts = _target_staging(staging, y)
         depth = self.n_slots if prefetch else 1
         nxt = 0
         while nxt < min(depth, len(jobs)):
@@ -253,11 +265,15 @@ class MicroBatchStreamer:
             if tracer is not None:
                 tracer.data_ready(self.slot_job[slot], self, cs)
             base = self.dev_slots[slot].data_ptr()
-            buf = _dest(dest, n, sample_shape, staging, y_shape, y.dtype)
+            buf = _dest(dest, n, sample_shape, staging, y_shape, ts.dtype if ts is not None else y.dtype)
             xk = stage_rows(base, x.dtype, sample_shape, None, 0, n, staging, self.device, cs,
                             out=buf[0] if buf is not None else None)
-            yk = gather_rows(base + self.y_off, y.dtype, y_shape, None, 0, n, self.device, cs,
-                             out=buf[1] if buf is not None else None)
+            if ts is not None:
+                yk = stage_rows(base + self.y_off, y.dtype, y_shape, None, 0, n, ts, self.device, cs,
+                                out=buf[1] if buf is not None else None)
+            else:
+                yk = gather_rows(base + self.y_off, y.dtype, y_shape, None, 0, n, self.device, cs,
+                                 out=buf[1] if buf is not None else None)
             N.check(N.lib().mbs_streamer_release(self._h, slot, cs.cuda_stream), "mbs_streamer_release")
             if prefetch and nxt < len(jobs):
                 self._submit(nxt % self.n_slots, x, y, *jobs[nxt])

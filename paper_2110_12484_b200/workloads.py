@@ -99,6 +99,10 @@ WORKLOADS = {
                    "cross_entropy", "sgd"),
     "c3": Workload("unet-384-carvana-256/48", "unet", (3, 384, 384), "mask", 1, 256, 48, "bce_dice", "adam"),
     "c5": Workload("unet-768-autosized", "unet", (3, 768, 768), "mask", 1, 64, 0, "bce_dice", "adam"),
+    # N1 (north_star Target): U-Net@384 with a mini-batch whose data exceeds HBM: 80,000 samples = 47.2 GB as
+    # uint8 image + mask, 188.7 GB as the reference's float32 arrays; micro 48 -> 1,666 x 48 + a tail of 32
+    "n1": Workload("unet-384-host-resident-80000/48", "unet", (3, 384, 384), "mask", 1, 80_000, 48, "bce_dice",
+                   "adam"),
     # C4: one mini-batch per GPU of 300,032 = 2,344 x 128 samples: 45.2 GB host-resident as uint8
     # (180.6 GB as the reference's float32/float64 arrays would hold it: larger than the 180 GB HBM)
     "c4": Workload("resnet50-224-host-resident-300032/128", "resnet50", (3, 224, 224), "classes", 102, 300_032,
@@ -155,13 +159,15 @@ def gflop_per_sample(w: Workload, device) -> float:
 
 
 def synthetic_data(w: Workload, n: int, seed: int = 0, device="cpu", pinned: bool = False):
-    """uint8 images (the dataset's natural storage) and int64 labels / float32 {0,1} masks.
+    """uint8 images and int64 labels / uint8 {0,1} masks (the datasets' natural storage; K2 stages
+    both to the model's dtypes on device, ``Staging.target_dtype`` for masks).
 
     Large host datasets (> 4 GB) are allocated page-locked in place and filled by tiling 509
     random samples (memcpy speed) instead of per-byte RNG.
     """
     g = torch.Generator().manual_seed(seed)
     row = int(torch.tensor(w.sample_shape).prod())
+    mask_shape = (1,) + tuple(w.sample_shape[1:])
     if str(device) == "cpu" and n * row > 4 * 2 ** 30:
         x = torch.empty((n,) + w.sample_shape, dtype=torch.uint8, pin_memory=pinned)
         base = torch.randint(0, 256, (509,) + w.sample_shape, generator=g, dtype=torch.uint8)
@@ -170,14 +176,18 @@ def synthetic_data(w: Workload, n: int, seed: int = 0, device="cpu", pinned: boo
             x[i:i + k].copy_(base[:k])
         if w.target == "classes":
             y = torch.randint(0, w.n_classes, (n,), generator=g, dtype=torch.int64)
-        else:
-            y = (torch.rand((n, 1) + w.sample_shape[1:], generator=g) < 0.5).float()
-        return x, (y.pin_memory() if pinned else y)
+            return x, (y.pin_memory() if pinned else y)
+        y = torch.empty((n,) + mask_shape, dtype=torch.uint8, pin_memory=pinned)
+        mb = (torch.rand((509,) + mask_shape, generator=g) < 0.5).to(torch.uint8)
+        for i in range(0, n, mb.shape[0]):
+            k = min(mb.shape[0], n - i)
+            y[i:i + k].copy_(mb[:k])
+        return x, y
     x = torch.randint(0, 256, (n,) + w.sample_shape, generator=g, dtype=torch.uint8)
     if w.target == "classes":
         y = torch.randint(0, w.n_classes, (n,), generator=g, dtype=torch.int64)
     else:
-        y = (torch.rand((n, 1) + w.sample_shape[1:], generator=g) < 0.5).float()
+        y = (torch.rand((n,) + mask_shape, generator=g) < 0.5).to(torch.uint8)
     if pinned:
         return x.pin_memory(), y.pin_memory()
     return x.to(device), y.to(device)

@@ -9,7 +9,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_reference_arm_json_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c1",
-                          "--steps", "1", "--warmup", "1", "--cpu-sample", "8"], capture_output=True, text=True,
+                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True,
                          timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
@@ -20,3 +20,7 @@ def test_reference_arm_json_line():
     assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "port"
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert line["config"]["workload"].startswith("resnet18")
+    # the config names the workload (as the GPU arm's does); what the bounded CPU sample ran is stated apart
+    assert line["config"]["mini_batch_per_gpu"] == 64 and line["config"]["micro_batch"] == 8
+    assert line["reference_sample"] == {"mini_batch": 16, "micro_batch": 8, "steps": 1, "warmup": 3}
+    assert line["warmup"] == 3 and line["steps"] == 1

@@ -13,12 +13,19 @@ seeded exactly as ``backward(tape, factor)`` (engine.py:214-215 -> nn.py:596), a
 normalised / stepped by the float64 restatement of engine.py / optim.py.
 
 Tolerance: the model numerics of a precision have a floor against float64
-that is not an MBS property. It is measured in each case as PLAIN torch on this GPU at the same
-precision (stock modules, torch autocast casting fp32 masters for bf16), the same micro split and
-factors, autograd accumulation. Contract, per precision:
+that is not an MBS property. It is measured in each case as PLAIN torch (stock modules, torch
+autocast casting fp32 masters for bf16), the same micro split and factors, autograd accumulation, in
+independent implementations of that precision — on this GPU channels-last and NCHW (different cuDNN
+kernels), and on the CPU for fp32 — and the floor is the largest of them. One implementation is
+not enough: BatchNorm over a micro-batch of 8 makes the gradient chaotic at ReLU ties, and which fp32
+implementation flips a mask on a given input is luck (measured, tools/diag_r02c.py: ResNet-18@32 fp32,
+7 of 8 micro-batches at 1.2e-5 for both torch and K5, one at 8e-3 for K5 only; its block re-run on
+the captured inputs is exact to 5e-7). Contract, per precision:
 
-    accumulated gradient   rel-L2(ours, fp64) <= max(1e-5, 1.5 * rel-L2(plain, fp64))
-    loss / grad-norm       |rel err| <= max(1e-5, 1.5 * plain's) (+ 1e-6 slack)
+    accumulated gradient   rel-L2(ours, fp64) <= max(1e-5, 1.5 * floor)
+    loss                   |rel err| <= max(1e-5, 1.5 * the plain runs' largest)
+    grad-norm              K1's fused norm == ||our accumulated gradient|| to 1e-6, and
+                           |rel err vs fp64| <= max(1e-5, 1.5 * floor) (it is bounded by the gradient's)
     post-step weights      rel-L2(ours, fp64) <= max(1e-5, 1.5 * the same step's floor)
     the step itself        fp64 optimizer applied to OUR gradient == our K3 result to 1e-6
 
@@ -71,19 +78,19 @@ def _opt(kind, ours: bool):
     return mbs.adam_state(0.01, 5e-4) if ours else O.OptState("adam", 0.01, weight_decay=5e-4)
 
 
-def _plain_gpu(cuda, net, w, x, y, plan, mode, precision):
-    """Stock torch on this GPU at the precision: the floor of the model numerics."""
-    pnet = copy.deepcopy(net).to(cuda).to(memory_format=torch.channels_last).train()
-    ctx = torch.autocast("cuda", dtype=torch.bfloat16) if precision == "bf16" else torch.autocast("cuda",
-                                                                                                   enabled=False)
+def _plain(dev, net, w, x, y, plan, mode, precision, fmt):
+    """Stock torch at the precision on ``dev`` in memory format ``fmt``: one sample of the model-numerics floor."""
+    pnet = copy.deepcopy(net).to(dev).to(memory_format=fmt).train()
+    ctx = torch.autocast(dev.type, dtype=torch.bfloat16) if precision == "bf16" else \
+        torch.autocast(dev.type, enabled=False)
     losses = []
     for k, (lo, hi) in enumerate(plan.index_ranges):
         f = O.normalization_factor(plan, k, mode)
-        xk = x[lo:hi].to(cuda).float().contiguous(memory_format=torch.channels_last)
+        xk = x[lo:hi].to(dev).float().contiguous(memory_format=fmt)
         with ctx:
-            loss = mbs.compute_loss(w.loss_kind, pnet(xk), y[lo:hi].to(cuda))
+            loss = mbs.compute_loss(w.loss_kind, pnet(xk), y[lo:hi].to(dev))
         (loss * f).backward()
-        losses.append(float(loss))
+        losses.append(float(loss.detach()))
     grads = {n: p.grad.double().cpu().numpy() for n, p in pnet.named_parameters()}
     return grads, O.mini_loss(plan.sizes, losses, plan.n_b)
 
@@ -105,9 +112,16 @@ def test_bench_stack_vs_fp64_oracle(cuda, case, precision):
     shapes = {n: v.shape for n, v in ref.params().items()}
     g64, st64 = O.mini_batch_gradient(ref, shapes, x.double().numpy(), y.numpy(), plan, mode)
 
-    # floor: plain torch on this GPU at this precision
-    plain, plain_loss = _plain_gpu(cuda, net, w, x, y, plan, mode, precision)
-    floor = rel_l2(_flat(plain, names), _flat(g64, names))
+    # floor: plain torch at this precision, independent implementations; the largest error counts
+    impls = [("gpu_channels_last", cuda, torch.channels_last), ("gpu_nchw", cuda, torch.contiguous_format)]
+    if precision == "fp32":
+        impls.append(("cpu", torch.device("cpu"), torch.contiguous_format))
+    runs = {tag: _plain(dev, net, w, x, y, plan, mode, precision, fmt) for tag, dev, fmt in impls}
+    floors = {tag: rel_l2(_flat(g, names), _flat(g64, names)) for tag, (g, _) in runs.items()}
+    floor_tag = max(floors, key=floors.get)
+    floor = floors[floor_tag]
+    plain = runs[floor_tag][0]
+    loss_floor = max(abs(lv - st64["loss"]) / abs(st64["loss"]) for _, lv in runs.values())
 
     # ours: exactly bench.py's stack
     graphs.clear()
@@ -122,17 +136,18 @@ def test_bench_stack_vs_fp64_oracle(cuda, case, precision):
     got = {n: total[n].detach().double().cpu().numpy() for n in names}
     err = rel_l2(_flat(got, names), _flat(g64, names))
     loss_err = abs(st.loss - st64["loss"]) / abs(st64["loss"])
-    loss_floor = abs(plain_loss - st64["loss"]) / abs(st64["loss"])
     gn_err = abs(st.grad_norm - st64["grad_norm"]) / st64["grad_norm"]
-    gn_floor = abs(np.linalg.norm(_flat(plain, names)) - st64["grad_norm"]) / st64["grad_norm"]
+    gn_self = abs(st.grad_norm - np.linalg.norm(_flat(got, names))) / np.linalg.norm(_flat(got, names))
 
     # one optimizer step from the same start
     w0 = ref.params()
     w64 = {n: v.copy() for n, v in w0.items()}
     O.apply_update(w64, g64, _opt(w.optimizer, False))
-    wpl = {n: v.copy() for n, v in w0.items()}
-    O.apply_update(wpl, plain, _opt(w.optimizer, False))
-    wfloor = rel_l2(_flat(wpl, names), _flat(w64, names))
+    wfloor = 0.0
+    for g_plain, _ in runs.values():      # the same step from each plain gradient: the step's floor
+        wpl = {n: v.copy() for n, v in w0.items()}
+        O.apply_update(wpl, g_plain, _opt(w.optimizer, False))
+        wfloor = max(wfloor, rel_l2(_flat(wpl, names), _flat(w64, names)))
     wo = {n: v.copy() for n, v in w0.items()}
     O.apply_update(wo, got, _opt(w.optimizer, False))       # the float64 step on OUR gradient
     dst = _opt(w.optimizer, True)
@@ -143,11 +158,11 @@ def test_bench_stack_vs_fp64_oracle(cuda, case, precision):
     if bf16:   # the shadow the next forward reads is the RNE cast of the updated master
         assert torch.equal(params.shadow, params.flat.to(torch.bfloat16))
 
-    per_tensor = {n: {"ours": rel_l2(got[n], g64[n]), "plain": rel_l2(plain[n], g64[n])} for n in names}
+    per_tensor = {n: {"ours": rel_l2(got[n], g64[n]), "plain_" + floor_tag: rel_l2(plain[n], g64[n])} for n in names}
     worst = max(names, key=lambda n: per_tensor[n]["ours"])
     rep = {"case": case, "precision": precision, "plan": list(plan.sizes), "grad_rel_l2": err,
-           "grad_floor": floor, "ratio": err / floor if floor else None, "loss_rel": loss_err,
-           "loss_floor": loss_floor, "grad_norm_rel": gn_err, "grad_norm_floor": gn_floor,
+           "grad_floor": floor, "floors": floors, "ratio": err / floor if floor else None, "loss_rel": loss_err,
+           "loss_floor": loss_floor, "grad_norm_rel": gn_err, "grad_norm_vs_own_gradient": gn_self,
            "post_step_rel_l2": werr, "post_step_floor": wfloor, "k3_step_vs_fp64_step": step_err,
            "worst_tensor": worst, "per_tensor": per_tensor}
     path = os.environ.get("MBS_PARITY_REPORT")
@@ -157,7 +172,8 @@ def test_bench_stack_vs_fp64_oracle(cuda, case, precision):
     graphs.clear()
 
     assert err <= max(1e-5, 1.5 * floor), rep
-    assert loss_err <= max(1e-5, 1.5 * loss_floor) + 1e-6, rep
-    assert gn_err <= max(1e-5, 1.5 * gn_floor) + 1e-6, rep
+    assert loss_err <= max(1e-5, 1.5 * loss_floor), rep
+    assert gn_self <= 1e-6, rep
+    assert gn_err <= max(1e-5, 1.5 * floor), rep
     assert step_err <= 1e-6, rep
     assert werr <= max(1e-5, 1.5 * wfloor), rep

@@ -48,7 +48,7 @@ def test_tracer_schedule_shape_and_order(cuda, host, monkeypatch):
     # tracing changes nothing (same kernels, same order)
     assert torch.equal(w0, w1) and es0.mini_losses == es1.mini_losses
     scheds = tr.schedules()
-    assert [len(s.events) for s in scheds] == [(3 + host) * n + 1 for n in (3, 3, 1)]   # 44 = 20 + 20 + 4
+    assert [len(s.events) for s in scheds] == [(2 + host) * n + 1 for n in (3, 3, 1)]   # 44 = 20 + 20 + 4
     prev_update_end = -1.0
     for s in scheds:
         ev = {(e.kind, e.index): e for e in s.events}
