@@ -13,8 +13,8 @@ from . import _native, bn, pool, stem
 from .engine import (NORMALIZATION_MODES, EpochStats, GradientAccumulator, MicroBatchPlan, MiniBatchStats,
                      accumulate, make_streamer, mini_batch_gradient, normalization_factor, normalize_loss,
                      plan_split, train_epoch, train_mini_batch)
-from .errors import (AccumulatorOverflowError, ConfigError, GradientKeyMismatchError, ModelDoesNotFitError,
-                     NonFiniteError, ShapeCompositionError, TapeConsumedError)
+from .errors import (AccumulatorOverflowError, ConfigError, GradientKeyMismatchError, IdxFormatError,
+                     ModelDoesNotFitError, NonFiniteError, ShapeCompositionError, TapeConsumedError)
 from .losses import LossValue, accuracy, compute_loss, dice_coefficient, iou
 from .optim import OptimizerState, adam_state, adam_step, apply_update, linear_lr, sgd_state, sgd_step
 from .rng import epoch_order, named_stream, stream_key
@@ -24,7 +24,7 @@ from .tensor import GradientSet, ParameterSet, ParamLayout
 __all__ = [
     "NORMALIZATION_MODES", "EpochStats", "GradientAccumulator", "MicroBatchPlan", "MiniBatchStats", "accumulate",
     "make_streamer", "mini_batch_gradient", "normalization_factor", "normalize_loss", "plan_split", "train_epoch",
-    "train_mini_batch", "AccumulatorOverflowError", "ConfigError", "GradientKeyMismatchError",
+    "train_mini_batch", "AccumulatorOverflowError", "ConfigError", "GradientKeyMismatchError", "IdxFormatError",
     "ModelDoesNotFitError", "NonFiniteError", "ShapeCompositionError", "TapeConsumedError", "LossValue",
     "accuracy", "compute_loss", "dice_coefficient", "iou", "OptimizerState", "adam_state", "adam_step",
     "apply_update", "linear_lr", "sgd_state", "sgd_step", "epoch_order", "named_stream", "stream_key",

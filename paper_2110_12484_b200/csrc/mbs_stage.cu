@@ -386,10 +386,118 @@ k_stage_nhwc_bulk(const uint8_t* __restrict__ src, const int64_t* __restrict__ r
     if (tid == 0) bulk_wait_all();
 }
 
+// ---------------------------------------------------------------------------------------------
+// NCHW u8 -> NHWC, bulk-async, over the FLATTENED pixel space of the micro-batch with a balanced split:
+// CTA b owns the contiguous output pixels [b*per_cta, (b+1)*per_cta) (per_cta a multiple of 16 chosen so
+// that grid = the resident CTAs), walked in tiles of TP pixels through a kFlatStages-deep ring. A tile's
+// source planes may cross row boundaries (rows are gathered / strided in the source, contiguous in the
+// NHWC destination), so each plane is fetched as one bulk copy per row segment. Compared with the per-row
+// tiling of k_stage_nhwc_bulk there is no ragged last tile per row and no CTA doing one tile more than
+// another (C2: 24.5 tiles per row, 4.3 tiles per CTA -> 18 % of the CTAs ran a fifth tile).
+// ---------------------------------------------------------------------------------------------
+constexpr int kFlatStages = 4;
+
+template <int TP, int C, typename TO>
+constexpr size_t flat_smem_bytes() {
+    return (size_t)kFlatStages * C * TP + 2 * (size_t)TP * C * sizeof(TO);
+}
+
+template <int OUT, int C, int TP>
+__global__ void __launch_bounds__(kStageThreads)
+k_stage_nhwc_flat(const uint8_t* __restrict__ src, const int64_t* __restrict__ rows, int64_t row0, int64_t HW,
+                  int64_t total_px, int64_t per_cta, typename Out<OUT>::T* __restrict__ dst) {
+    using TO = typename Out<OUT>::T;
+    constexpr int PX = TP / kStageThreads;
+    static_assert(PX == 8 || PX == 16, "tile must give 8 or 16 pixels per thread");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[kFlatStages];
+    uint8_t* in = smem_raw;                                                       // [S][C][TP] planes
+    TO* out = reinterpret_cast<TO*>(smem_raw + (size_t)kFlatStages * C * TP);     // [2][TP*C] NHWC tiles
+    const int tid = threadIdx.x;
+    const int64_t begin = (int64_t)blockIdx.x * per_cta;
+    const int64_t end = min(total_px, begin + per_cta);
+    const int64_t n_mine = end > begin ? (end - begin + TP - 1) / TP : 0;
+
+    auto issue = [&](int64_t i) {                         // elected thread: tile i's planes -> stage i % S
+        const int64_t p0 = begin + i * TP;
+        const int npx = (int)min((int64_t)TP, end - p0);
+        const int s = (int)(i % kFlatStages);
+        mbar_expect_tx(&full[s], (uint32_t)(C * npx));
+        int done = 0;
+        while (done < npx) {                              // one bulk copy per plane per row segment
+            const int64_t p = p0 + done;
+            const int64_t r = p / HW, off = p - r * HW;
+            const int seg = (int)min((int64_t)(npx - done), HW - off);
+            const uint8_t* base = src + src_row(rows, row0, r) * (int64_t)C * HW + off;
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                bulk_load(in + ((size_t)s * C + c) * TP + done, base + c * HW, (uint32_t)seg, &full[s]);
+            done += seg;
+        }
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < kFlatStages; ++s) mbar_init(&full[s], 1);
+        mbar_init_fence();
+        for (int64_t i = 0; i < min((int64_t)kFlatStages, n_mine); ++i) issue(i);
+    }
+    __syncthreads();
+
+    for (int64_t i = 0; i < n_mine; ++i) {
+        const int64_t p0 = begin + i * TP;
+        const int npx = (int)min((int64_t)TP, end - p0);
+        const int s = (int)(i % kFlatStages);
+        TO* o = out + (size_t)(i & 1) * TP * C;
+        if (tid == 0) bulk_wait_read<1>();                // the store of tile i-2 has finished reading out[i&1]
+        mbar_wait(&full[s], (uint32_t)((i / kFlatStages) & 1));
+        __syncthreads();
+        const uint8_t* pl = in + (size_t)s * C * TP;
+        const int q0 = tid * PX;
+        if (q0 + PX <= npx) {
+            uint32_t w[C][PX / 4];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                if constexpr (PX == 16) {
+                    const uint4 q = *reinterpret_cast<const uint4*>(pl + c * TP + q0);
+                    w[c][0] = q.x; w[c][1] = q.y; w[c][2] = q.z; w[c][3] = q.w;
+                } else {
+                    const uint2 q = *reinterpret_cast<const uint2*>(pl + c * TP + q0);
+                    w[c][0] = q.x; w[c][1] = q.y;
+                }
+            }
+            constexpr int per = 16 / (int)sizeof(TO);
+            uint4* d16 = reinterpret_cast<uint4*>(o + (size_t)q0 * C);
+#pragma unroll
+            for (int v = 0; v < PX * C / per; ++v) {
+                TO e[per];
+#pragma unroll
+                for (int j = 0; j < per; ++j) {
+                    const int k = v * per + j, px = k / C, c = k % C;
+                    e[j] = Out<OUT>::cvt((float)((w[c][px >> 2] >> ((px & 3) * 8)) & 0xFFu));
+                }
+                uint4 q;
+                memcpy(&q, e, 16);
+                d16[v] = q;
+            }
+        } else {
+            for (int q = q0; q < npx && q < q0 + PX; ++q)
+                for (int c = 0; c < C; ++c) o[q * C + c] = Out<OUT>::cvt((float)pl[c * TP + q]);
+        }
+        fence_proxy_async_smem();
+        __syncthreads();                                  // stage s consumed, out[i&1] complete
+        if (tid == 0) {
+            bulk_store(dst + p0 * C, o, (uint32_t)(npx * C * sizeof(TO)));
+            if (i + kFlatStages < n_mine) issue(i + kFlatStages);
+        }
+    }
+    if (tid == 0) bulk_wait_all();
+}
+
 static int stage_path() {
-    // A/B only: 0 = per-row, 1 = grid-stride vec, 2 = smem, 3 = bulk-async (default)
+    // A/B only: 0 = per-row, 1 = grid-stride vec, 2 = smem, 3 = bulk-async per row, 4 = bulk-async over the
+    // flattened, evenly split pixel space (default)
     const char* e = getenv("MBS_K2_PATH");
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 4;
 }
 
 static int bulk_tile() {
@@ -432,6 +540,28 @@ static int launch_bulk(const uint8_t* s, const int64_t* rows, int64_t row0, int6
     const int grid = (int)std::min<int64_t>(total, (int64_t)sm_count() * per_sm);
     kern<<<grid, kStageThreads, sm, st>>>(s, rows, row0, HW, tpr, total, d);
     MBS_CK_LAUNCH("k_stage_nhwc_bulk");
+    return MBS_OK;
+}
+
+template <int OUT, int C, int TP>
+static int launch_flat(const uint8_t* s, const int64_t* rows, int64_t row0, int64_t n_rows, int64_t HW,
+                       typename Out<OUT>::T* d, cudaStream_t st) {
+    using TO = typename Out<OUT>::T;
+    auto kern = k_stage_nhwc_flat<OUT, C, TP>;
+    constexpr size_t sm = flat_smem_bytes<TP, C, TO>();
+    static int per_sm = 0;
+    if (!per_sm) {
+        MBS_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        MBS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStageThreads, sm));
+        if (per_sm < 1) per_sm = 1;
+    }
+    const int64_t total = n_rows * HW;
+    const int64_t resident = (int64_t)sm_count() * per_sm;
+    int64_t per_cta = (total + resident - 1) / resident;
+    per_cta = std::max<int64_t>(16, (per_cta + 15) / 16 * 16);   // 16-byte aligned bulk copies
+    const int grid = (int)((total + per_cta - 1) / per_cta);
+    kern<<<grid, kStageThreads, sm, st>>>(s, rows, row0, HW, total, per_cta, d);
+    MBS_CK_LAUNCH("k_stage_nhwc_flat");
     return MBS_OK;
 }
 
@@ -485,6 +615,14 @@ static int stage_typed(const void* src, const int64_t* rows, int64_t row0, int64
                               (da % 16 == 0) && ((kPix * sizeof(TO)) % 16 == 0);
         const int path = stage_path();
         if constexpr (sizeof(TI) == 1) {
+            if (path == 4 && nhwc && C <= 4 && HW % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
+                is_device_memory(src)) {
+                switch (C) {
+                    case 2: return launch_flat<OUT, 2, 2048>(s, rows, row0, n_rows, HW, d, st);
+                    case 3: return launch_flat<OUT, 3, 2048>(s, rows, row0, n_rows, HW, d, st);
+                    default: return launch_flat<OUT, 4, 2048>(s, rows, row0, n_rows, HW, d, st);
+                }
+            }
             if (path == 3 && nhwc && C <= 4 && HW % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
                 is_device_memory(src)) {
                 const bool small = OUT == MBS_F32 || bulk_tile() == 2048;   // f32 tiles: 2048 px keeps 2 CTAs/SM
@@ -498,7 +636,7 @@ static int stage_typed(const void* src, const int64_t* rows, int64_t row0, int64
                 }
             }
         }
-        if ((path == 2 || path == 3) && nhwc && C <= 4 && (HW * (int64_t)sizeof(TI)) % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
+        if ((path == 2 || path == 3 || path == 4) && nhwc && C <= 4 && (HW * (int64_t)sizeof(TI)) % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
             ((int64_t)kTilePx * C * sizeof(TO)) % 16 == 0 && (HW * C * (int64_t)sizeof(TO)) % 16 == 0) {
             const int64_t tpr = (HW + kTilePx - 1) / kTilePx, total = n_rows * tpr;
             const size_t sm = (size_t)kTilePx * C * sizeof(TO);

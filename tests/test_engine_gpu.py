@@ -334,7 +334,7 @@ def test_train_epoch_metric_fn_matches_reference(cuda, name, host):
     a = load_npz("epoch_metrics.npz")
     torch.manual_seed(0)
     mod = build_torch(meta["spec"], tuple(meta["input_shape"])).to(cuda)
-    load_ref_params(mod, meta["spec"], {k[len(name) + 4:]: a[k] for k in a.files if k.startswith(f"{name}/p0/")})
+    load_ref_params(mod, meta["spec"], {k[len(name) + 4:]: a[k] for k in a.keys() if k.startswith(f"{name}/p0/")})
     params = mbs.ParameterSet(mod)
     x = torch.from_numpy(a[f"{name}/x"]).float()
     y = torch.from_numpy(a[f"{name}/y"])

@@ -27,7 +27,7 @@ def _classes(n, seed):
     proto = torch.rand((10, 3, 4, 4), generator=torch.Generator().manual_seed(123)) * 160 + 40
     y = torch.randint(0, 10, (n,), generator=g)
     img = torch.nn.functional.interpolate(proto[y], size=(32, 32), mode="nearest")
-    img = img + torch.randn(img.shape, generator=g) * 40
+    img = img + torch.randn(img.shape, generator=g) * 110      # heavy noise: held-out accuracy well below 100 %
     return img.clamp(0, 255).to(torch.uint8), y
 
 
@@ -38,7 +38,7 @@ def _shapes(n, seed, s=64):
     c = torch.rand((n, 2), generator=g) * s * 0.6 + s * 0.2
     r = torch.rand((n,), generator=g) * s * 0.2 + s * 0.1
     m = ((yy[None] - c[:, 0, None, None]) ** 2 + (xx[None] - c[:, 1, None, None]) ** 2 < r[:, None, None] ** 2)
-    img = 60 + 120 * m[:, None].float().expand(n, 3, s, s) + torch.randn((n, 3, s, s), generator=g) * 30
+    img = 60 + 60 * m[:, None].float().expand(n, 3, s, s) + torch.randn((n, 3, s, s), generator=g) * 90
     return img.clamp(0, 255).to(torch.uint8), m[:, None].to(torch.uint8)
 
 
@@ -59,7 +59,8 @@ def _train(cuda, net0, x, y, loss_kind, opt, mini, micro, epochs, metric):
 @torch.no_grad()
 def _eval(net, x, y, fn):
     net.eval()
-    out = net(x.float().contiguous(memory_format=torch.channels_last))
+    with torch.autocast("cuda", dtype=torch.bfloat16):      # the bf16 shadow weights, as in training
+        out = net(x.float().contiguous(memory_format=torch.channels_last))
     net.train()
     return fn(out.float(), y)
 
@@ -75,7 +76,7 @@ def test_resnet18_accuracy_with_and_without_mbs(cuda):
         net, es = _train(cuda, net0, x.to(cuda), y.to(cuda), "cross_entropy", "sgd", 64, micro, 3, mbs.accuracy)
         acc[micro] = (_eval(net, xt, yt, mbs.accuracy), es.mini_metrics[-1])
     print("held-out accuracy: MBS(micro 8) %.4f  no-MBS %.4f" % (acc[8][0], acc[None][0]))
-    assert acc[None][0] >= 0.9, "the no-MBS baseline did not learn the task"
+    assert acc[None][0] >= 0.5, "the no-MBS baseline did not learn the task"
     assert abs(acc[8][0] - acc[None][0]) <= 0.05
 
 
@@ -93,5 +94,5 @@ def test_unet_iou_with_and_without_mbs(cuda):
         net, es = _train(cuda, net0, x.to(cuda), y.to(cuda), "bce_dice", "adam", 16, micro, 4, iou)
         res[micro] = _eval(net, xt, yt, iou)
     print("held-out IoU: MBS(micro 4) %.4f  no-MBS %.4f" % (res[4], res[None]))
-    assert res[None] >= 0.8, "the no-MBS baseline did not learn the task"
+    assert res[None] >= 0.5, "the no-MBS baseline did not learn the task"
     assert abs(res[4] - res[None]) <= 0.05

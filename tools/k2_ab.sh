@@ -1,7 +1,7 @@
 #!/bin/bash
 # K2 staging A/B: MBS_K2_PATH 0 = per-row kernels, 1 = grid-stride vector kernel, 2 = smem-staged NHWC,
 # 3 = bulk-async (TMA) ring; MBS_K2_TILE 2048|4096 for path 3
-for pt in 1:4096 2:4096 3:4096 3:2048; do
+for pt in 2:4096 3:2048 4:2048; do
   MBS_K2_PATH=${pt%%:*} MBS_K2_TILE=${pt##*:} python tools/kbench.py --iters 30 > /tmp/kb.json 2>&1
   python - "$pt" <<'PY'
 import json, sys
