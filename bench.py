@@ -122,6 +122,45 @@ def _dist():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+class SharedHostPool:
+    """The image pool of a multi-rank run, ONE copy per node: local rank 0 writes it into a shared file
+    (``/dev/shm``, else ``/tmp``), every local rank maps it and page-locks its mapping (cudaHostRegister), and
+    each rank streams it in its own rank-keyed order (dp.DataParallelMBS.train_epoch). C4 at 8 ranks would
+    otherwise pin 8 x 45.2 GB = 361 GB of uint8 on a host with ~200 GB of RAM."""
+
+    def __init__(self, w, n: int, local_rank: int, barrier):
+        from paper_2110_12484_b200.workloads import synthetic_data
+        self.shape = (n,) + tuple(w.sample_shape)
+        self.nbytes = int(np.prod(self.shape))
+        base = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
+        st = os.statvfs(base)
+        if st.f_bavail * st.f_frsize < 1.05 * self.nbytes:
+            base = "/tmp"
+        self.path = os.path.join(base, f"mbs_bench_pool_{w.name.replace('/', '_')}_{n}_{os.getppid()}.u8")
+        self.owner = local_rank == 0
+        if self.owner:
+            x = torch.from_file(self.path, shared=True, size=self.nbytes, dtype=torch.uint8).view(self.shape)
+            pool, _ = synthetic_data(w, min(n, 509), seed=0)
+            for i in range(0, n, pool.shape[0]):
+                k = min(pool.shape[0], n - i)
+                x[i:i + k].copy_(pool[:k])
+            del x
+        barrier()
+        self.x = torch.from_file(self.path, shared=True, size=self.nbytes, dtype=torch.uint8).view(self.shape)
+        torch.cuda.cudart().cudaHostRegister(self.x.data_ptr(), self.nbytes, 0)
+        self.where = base
+
+    def close(self, barrier):
+        try:
+            torch.cuda.cudart().cudaHostUnregister(self.x.data_ptr())
+        except Exception:
+            pass
+        del self.x
+        barrier()
+        if self.owner and os.path.exists(self.path):
+            os.unlink(self.path)
+
+
 def workload_config(w, n_b: int, n_mu: int, ws: int, model_ops: str) -> dict:
     """The ``config`` object of BOTH arms' JSON lines (the workload; what a sample of it ran is separate)."""
     from paper_2110_12484_b200 import engine
@@ -270,7 +309,15 @@ def run_gpu(args, w, ws, rank, local):
     row = int(np.prod(w.sample_shape)) + (int(np.prod(w.sample_shape[1:])) if w.target == "mask" else 8)
     d_minis = max(1, min(args.steps, HOST_DATA_CAP // (n_b * row)))
     t_data = time.perf_counter()
-    x_host, y_host = synthetic_data(w, d_minis * n_b, seed=rank, pinned=True)
+    pool = None
+    if ws > 1 and os.environ.get("MBS_SHARED_HOST_POOL", "1") != "0":
+        def _barrier():
+            torch.distributed.barrier()
+        pool = SharedHostPool(w, d_minis * n_b, local, _barrier)
+        x_host = pool.x
+        y_host = synthetic_data(w, d_minis * n_b, seed=rank, pinned=True)[1]      # per-rank labels / masks
+    else:
+        x_host, y_host = synthetic_data(w, d_minis * n_b, seed=rank, pinned=True)
     x_dev, y_dev = x_host.to(dev), y_host.to(dev)
     t_data = time.perf_counter() - t_data
     warm_small = min(n_b, 1024)          # e2e warm-up: one small mini-batch through the (already warm) stack
@@ -480,7 +527,10 @@ def run_gpu(args, w, ws, rank, local):
                    "host_dataset": {"mini_batches": d_minis, "samples": d_minis * n_b,
                                     "bytes": int(x_host.numel() * x_host.element_size() +
                                                  y_host.numel() * y_host.element_size()),
-                                    "pinned": True, "setup_s": t_data},
+                                    "pinned": True, "setup_s": t_data,
+                                    "images": ("one page-locked copy per node in %s, mapped by every rank; each "
+                                               "rank streams it in its own order" % pool.where) if pool else
+                                              "per rank, page-locked"},
                    "steps_are": "one mini-batch each; an epoch over the host dataset every "
                                 f"{d_minis} steps, reshuffled by epoch_index",
                    "warmup_is": f"{args.warmup} full mini-batches before the HBM-resident (value) run; 1 mini-batch "
@@ -519,6 +569,9 @@ def run_gpu(args, w, ws, rank, local):
     if rank == 0:
         print(json.dumps(line))
     if ws > 1:
+        if pool is not None:
+            del x_host
+            pool.close(torch.distributed.barrier)
         torch.distributed.destroy_process_group()
 
 
