@@ -18,6 +18,7 @@ from __future__ import annotations
 import argparse
 import csv
 import dataclasses
+import gc
 import io
 import json
 import math
@@ -299,6 +300,8 @@ def _probe_budget(cfg, x, y, dev):
     import torch
     from . import memory
     from .streamer import Staging, stage_rows
+    gc.collect()                                  # a previous run's graphs / tensors are not this model's
+    base = torch.cuda.memory_allocated(dev)
     torch.manual_seed(0)
     model = build_model(cfg).to(dev)
     if x.dim() == 4:
@@ -315,7 +318,7 @@ def _probe_budget(cfg, x, y, dev):
     n = min(8, x.shape[0])
     probe = (max(1, n // 2), n) if n >= 2 else (1, 2)
     b = memory.measure_budget(model, make_batch, cfg.loss, optimizer_kind=cfg.optimizer,
-                              autocast_dtype=torch.bfloat16 if bf16 else None, probe=probe)
+                              autocast_dtype=torch.bfloat16 if bf16 else None, probe=probe, baseline_bytes=base)
     if cfg.capacity_bytes:
         b = memory.MemoryBudget(capacity_bytes=int(cfg.capacity_bytes), param_bytes=b.param_bytes,
                                 data_bytes_per_sample=b.data_bytes_per_sample,

@@ -643,7 +643,12 @@ __global__ void __launch_bounds__(kBnThreads, 2) k_bn_tma(
                     float d2[V];
                     BnIO<T, V>::load(ds + (size_t)kTmaTileBytes / sizeof(T) + o, d2);
 #pragma unroll
-                    for (int e = 0; e < V; ++e) dv[e] += d2[e];
+                    for (int e = 0; e < V; ++e) {
+                        dv[e] += d2[e];
+                        // bf16: the sum is rounded like torch's bf16 add, so the statistics and the stored
+                        // d_residual (read back by the elemt pass) see the same g
+                        if constexpr (sizeof(T) == 2) dv[e] = __bfloat162float(__float2bfloat16(dv[e]));
+                    }
                 }
                 if (RES) BnIO<T, V>::load(rsm + o, rv);
                 if ((KIND == 1 || KIND == 3) && RELU) {

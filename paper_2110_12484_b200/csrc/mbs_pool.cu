@@ -268,8 +268,14 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_fwd(const T* __restric
 // W2 = 1: non-overlapping windows tiling the input (the U-Net 2x2/s2 pools) — no window search.
 // W2 = 2: 3x3 windows, stride 2 (the ResNet stem): at most 2x2 candidate windows, unrolled and
 // predicated so their index/gradient loads are all in flight at once.
-// dy2 (nullable): a second gradient of y (the pooled activation has two consumers), added to dy in
-// fp32 per window before the gather sum — in fp32 exactly torch's (dy1 + dy2) then gather.
+// dy2 (nullable): a second gradient of y (the pooled activation has two consumers), added to dy per
+// window and rounded to T before the gather sum — exactly torch's (dy1 + dy2) in T, then gather.
+template <typename T>
+__device__ __forceinline__ float round_to(float v) {
+    if constexpr (sizeof(T) == 2) return __bfloat162float(__float2bfloat16(v));
+    else return v;
+}
+
 template <typename T, int V, typename I, int W2>
 __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restrict__ dy,
                                                               const uint8_t* __restrict__ idx, T* __restrict__ dx,
@@ -328,7 +334,7 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
                     float d2[V];
                     PoolIO<T, V>::load(reinterpret_cast<const T*>(&draw2[q2]), d2);
 #pragma unroll
-                    for (int i = 0; i < V; ++i) d[i] += d2[i];
+                    for (int i = 0; i < V; ++i) d[i] = round_to<T>(d[i] + d2[i]);
                 }
 #pragma unroll
                 for (int i = 0; i < V; ++i)
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
                 float d2[V];
                 PoolIO<T, V>::load(dy2 + o, d2);
 #pragma unroll
-                for (int i = 0; i < V; ++i) d[i] += d2[i];
+                for (int i = 0; i < V; ++i) d[i] = round_to<T>(d[i] + d2[i]);
             }
 #pragma unroll
             for (int i = 0; i < V; ++i)
@@ -369,7 +375,7 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd(const T* __restric
                         float d2[V];
                         PoolIO<T, V>::load(dy2 + o, d2);
 #pragma unroll
-                        for (int i = 0; i < V; ++i) d[i] += d2[i];
+                        for (int i = 0; i < V; ++i) d[i] = round_to<T>(d[i] + d2[i]);
                     }
 #pragma unroll
                     for (int i = 0; i < V; ++i)
@@ -429,7 +435,7 @@ __global__ void __launch_bounds__(kPoolThreads) k_maxpool_bwd_blk(const T* __res
                 float d2[V];
                 PoolIO<T, V>::load(reinterpret_cast<const T*>(&dr2[w]), d2);
 #pragma unroll
-                for (int i = 0; i < V; ++i) d[w][i] += d2[i];
+                for (int i = 0; i < V; ++i) d[w][i] = round_to<T>(d[w][i] + d2[i]);
             }
         }
 #pragma unroll

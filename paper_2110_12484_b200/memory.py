@@ -93,14 +93,16 @@ def _probe_peak(model, make_batch, n: int, loss_kind: str, autocast_dtype, devic
 
 
 def measure_budget(model: torch.nn.Module, make_batch, loss_kind: str, *, optimizer_kind: str = "sgd",
-                   autocast_dtype=None, probe: tuple = (2, 4), safety: float = 0.92, device=None) -> MemoryBudget:
+                   autocast_dtype=None, probe: tuple = (2, 4), safety: float = 0.92, device=None,
+                   baseline_bytes: int = 0) -> MemoryBudget:
     """Measured ``MemoryBudget`` for training ``model`` on this GPU.
 
     ``make_batch(n)`` returns a device (x, y) micro-batch of n samples already
     staged the way training will stage it. Per-sample bytes = slope of the
     probe peaks; fixed overhead = the intercept (cuDNN workspaces, the
     per-micro gradient tensors). ``safety`` keeps a margin for allocator
-    fragmentation.
+    fragmentation. ``baseline_bytes``: device bytes allocated before the model
+    was placed (other tensors of the process), excluded from what is resident.
     """
     device = torch.device(device or "cuda")
     model.train()
@@ -111,7 +113,7 @@ def measure_budget(model: torch.nn.Module, make_batch, loss_kind: str, *, optimi
     overhead = max(0, p1 - n1 * per_sample)
     free, _total = torch.cuda.mem_get_info(device)
     n_params = sum(p.numel() for p in model.parameters() if p.requires_grad)
-    held = torch.cuda.memory_allocated(device)
+    held = max(0, torch.cuda.memory_allocated(device) - int(baseline_bytes))
     capacity = int((free + held) * safety)
     # what is already resident (params, accumulator, optimizer state) is part of `held`
     resident = max(held, parameter_space_bytes(n_params, optimizer_kind))

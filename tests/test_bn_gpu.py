@@ -288,6 +288,21 @@ def test_k5_dual_output_bf16_no_worse_than_rounded_add(cuda, shape):
         assert ours <= max(1e-5, 1.05 * add), (k, ours, add)
 
 
+@pytest.mark.parametrize("shape", [(32, 256, 28, 28), (8, 2048, 7, 7)])
+def test_k5_dual_output_bf16_bit_identical_to_rounded_add(cuda, shape, monkeypatch):
+    """bf16: K5 rounds dy1 + dy2 to bf16 (torch's bf16 add) before the statistics and the stored
+    d_residual, so the dual path equals feeding the autograd-added gradient bit for bit (three-kernel
+    path on both sides: MBS_K5_FUSED=0)."""
+    monkeypatch.setenv("MBS_K5_FUSED", "0")
+    x, res, g1, w, b = _data(cuda, shape, torch.bfloat16, seed=33)
+    g2 = torch.randn_like(g1)
+    a = _run_dual(x, res, g1, g2, w, b, True)
+    c = _run(x, res, g1 + g2, w, b, True)
+    for k in a:
+        if a[k] is not None:
+            assert torch.equal(a[k], c[k]), k
+
+
 @pytest.mark.parametrize("arch", ["resnet18", "resnet50"])
 def test_fused_resnet_dual_handles_match_autograd_adds(cuda, arch, monkeypatch):
     """FusedResNet (block outputs handed on as two handles) vs the same fused model with autograd's

@@ -127,12 +127,14 @@ def test_unet_native_skips_match_plain(cuda):
 
 @pytest.mark.parametrize("case", [((4, 64, 112, 112), 3, 2, 1), ((2, 24, 17, 13), 3, 2, 1), ((3, 64, 48, 48), 2, 2, 0),
                                   ((2, 8, 9, 9), 3, 1, 1), ((2, 5, 11, 7), 2, 2, 0)])
-def test_k6_dual_output_fp32_bit_identical_to_summed_gradient(cuda, case):
-    """Dual output (the pooled activation feeds two consumers): K6 adds the two gradients in fp32 per
-    window before the gather — in fp32 exactly torch's (dy1 + dy2) then gather, so dx is bit-identical;
-    one unused handle (gradient None) is the single-output backward."""
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_k6_dual_output_bit_identical_to_summed_gradient(cuda, case, dtype):
+    """Dual output (the pooled activation feeds two consumers): K6 adds the two gradients per window and
+    rounds the sum to the activation dtype before the gather — exactly torch's (dy1 + dy2) then gather,
+    so dx is bit-identical in fp32 and bf16; one unused handle (gradient None) is the single-output
+    backward."""
     shape, k, s, p = case
-    x = torch.randn(shape, device=cuda).contiguous(memory_format=torch.channels_last)
+    x = torch.randn(shape, device=cuda).to(dtype).contiguous(memory_format=torch.channels_last)
     xa = x.clone().requires_grad_(True)
     y1, y2 = K6.max_pool2d(xa, k, s, p, dual=True)
     g1, g2 = torch.randn_like(y1), torch.randn_like(y1)

@@ -6,7 +6,7 @@ SEL_P="tests/test_dp_gpu.py::test_fused_peer_allreduce_two_ranks_one_gpu"
 for tool in memcheck racecheck synccheck initcheck; do
   for grp in K S P; do
     eval sel=\$SEL_$grp
-    timeout 1200 compute-sanitizer --tool $tool --kernel-name kns=3mbs --target-processes all --print-limit 50 \
+    timeout 700 compute-sanitizer --tool $tool --kernel-name kns=3mbs --target-processes all --print-limit 50 \
         --log-file gpurun_out/san_${tool}_${grp}_%p.log \
         python -m pytest $sel -q -m gpu -p no:cacheprovider > gpurun_out/san_${tool}_${grp}.out 2>&1
     echo "$tool $grp rc=$?" >> gpurun_out/san_summary.txt
