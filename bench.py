@@ -207,6 +207,24 @@ def run_cpu_reference(w, steps: int, warmup: int, sample_n_b: int, sample_n_mu: 
     return sps, threads, float(np.mean(times))
 
 
+def run_cpu_accumulate(shapes: dict, reps: int = 3):
+    """SURVEY §8(d) CPU baseline (3): the reference's GradientAccumulator.add (engine.py:117-128, restated
+    in the oracle: fp64 per-parameter ``sums[name] += g``) over one gradient of the workload's parameter
+    shapes; algorithmic bytes 24 B/param (read g, read sum, write sum, fp64). Returns (GB/s, s/add)."""
+    from oracle import mbs_oracle as O
+    acc = O.Accumulator(shapes)
+    rng = np.random.default_rng(0)
+    g = {n: rng.standard_normal(s) for n, s in shapes.items()}
+    n_params = sum(int(np.prod(s)) for s in shapes.values())
+    acc.begin(reps + 1)
+    acc.add(g)                                                 # warm-up (page faults)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        acc.add(g)
+    dt = (time.perf_counter() - t0) / reps
+    return 24 * n_params / dt / 1e9, dt
+
+
 def reference_arm(args, w, ws, rank):
     if rank != 0:
         return
@@ -566,6 +584,11 @@ def run_gpu(args, w, ws, rank, local):
         line["cpu_baseline"] = {"value": sps, "unit": "samples/s", "cores": cores, "kind": "port",
                                 "sample": f"1 mini-batch of {cpu_n_b} as micro {cpu_mu} (after 1 warm-up), {w.model} "
                                           f"float64 torch-CPU + NumPy MBS oracle, {step_s:.1f} s/step"}
+        shapes = {n: tuple(params[n].shape) for n in params.names()}
+        agbs, adt = run_cpu_accumulate(shapes)
+        line["cpu_baseline"]["accum_gbs"] = {"value": agbs, "unit": "GB/s", "cores": 1, "kind": "port",
+                                             "sample": f"GradientAccumulator.add of one {params.layout.n_params}-"
+                                                       f"parameter fp64 gradient, 24 B/param, {adt * 1e3:.0f} ms/add"}
     if rank == 0:
         print(json.dumps(line))
     if ws > 1:

@@ -57,6 +57,42 @@ __device__ __forceinline__ int64_t src_row(const int64_t* rows, int64_t row0, in
     return rows ? rows[r] : row0 + r;
 }
 
+// u8 -> float without the conversion pipe: PRMT places byte b of w under the exponent of 2^23
+// (0x4B0000vv = 2^23 + v, exact) and one FADD removes 2^23. I2F / F2F issue at a fraction of the
+// ALU rate on sm_100; on the staging kernels they were the binding resource (ncu: 1.5 conversion
+// instructions per staged element, 0.37 IPC, DRAM at 20 %).
+__device__ __forceinline__ float u8_lane_to_f32(uint32_t w, int b) {
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | (uint32_t)b)) - 8388608.0f;
+}
+
+// 16 bytes of interleaved NHWC output = elements [v*per, (v+1)*per) of a thread's PX pixels x C
+// channels, from its C planes of raw source bytes (w[c][px / 4], byte px % 4). Exact for every
+// output type: u8 values are integers below 256, so the float is exact, its bf16 (8 significant
+// bits) is its upper half word — one PRMT packs two — and its fp16 is exact as well.
+template <int OUT, int C, int NW>
+__device__ __forceinline__ uint4 u8_nhwc_vec16(const uint32_t (&w)[C][NW], int v) {
+    uint32_t q[4];
+    if constexpr (OUT == MBS_F32) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int k = v * 4 + j, px = k / C, c = k % C;
+            q[j] = __float_as_uint(u8_lane_to_f32(w[c][px >> 2], px & 3));
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int k0 = v * 8 + 2 * j, k1 = k0 + 1;
+            const float f0 = u8_lane_to_f32(w[k0 % C][(k0 / C) >> 2], (k0 / C) & 3);
+            const float f1 = u8_lane_to_f32(w[k1 % C][(k1 / C) >> 2], (k1 / C) & 3);
+            if constexpr (OUT == MBS_BF16)
+                q[j] = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x7632u);
+            else
+                q[j] = (uint32_t)Out<OUT>::cvt(f0) | ((uint32_t)Out<OUT>::cvt(f1) << 16);
+        }
+    }
+    return make_uint4(q[0], q[1], q[2], q[3]);
+}
+
 // Load kPix consecutive source elements as floats (vector path when aligned).
 template <typename TI>
 __device__ __forceinline__ void load_pix(const TI* p, float* v, bool vec) {
@@ -65,7 +101,7 @@ __device__ __forceinline__ void load_pix(const TI* p, float* v, bool vec) {
             const uint4 q = *reinterpret_cast<const uint4*>(p);
             const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = (float)((w[i >> 2] >> ((i & 3) * 8)) & 0xFFu);
+            for (int i = 0; i < 16; ++i) v[i] = u8_lane_to_f32(w[i >> 2], i & 3);
         } else if constexpr (sizeof(TI) == 8) {
 #pragma unroll
             for (int j = 0; j < kPix / 2; ++j) {
@@ -159,8 +195,7 @@ k_stage_nhwc(const TI* __restrict__ src, const int64_t* __restrict__ rows, int64
 template <typename TI>
 __device__ __forceinline__ float raw_elem(const uint4* raw, int i) {
     if constexpr (sizeof(TI) == 1) {
-        const uint32_t w = reinterpret_cast<const uint32_t*>(raw)[i >> 2];
-        return (float)((w >> ((i & 3) * 8)) & 0xFFu);
+        return u8_lane_to_f32(reinterpret_cast<const uint32_t*>(raw)[i >> 2], i & 3);
     } else if constexpr (sizeof(TI) == 4) {
         return reinterpret_cast<const float*>(raw)[i];
     } else {
@@ -361,17 +396,7 @@ k_stage_nhwc_bulk(const uint8_t* __restrict__ src, const int64_t* __restrict__ r
             constexpr int per = 16 / (int)sizeof(TO);     // outputs per 16-byte smem store
             uint4* d16 = reinterpret_cast<uint4*>(o + (size_t)q0 * C);
 #pragma unroll
-            for (int v = 0; v < PX * C / per; ++v) {
-                TO e[per];
-#pragma unroll
-                for (int j = 0; j < per; ++j) {
-                    const int k = v * per + j, px = k / C, c = k % C;
-                    e[j] = Out<OUT>::cvt((float)((w[c][px >> 2] >> ((px & 3) * 8)) & 0xFFu));
-                }
-                uint4 q;
-                memcpy(&q, e, 16);
-                d16[v] = q;
-            }
+            for (int v = 0; v < PX * C / per; ++v) d16[v] = u8_nhwc_vec16<OUT, C, PX / 4>(w, v);
         } else {
             for (int q = q0; q < npx && q < q0 + PX; ++q)
                 for (int c = 0; c < C; ++c) o[q * C + c] = Out<OUT>::cvt((float)pl[c * TP + q]);
@@ -465,20 +490,10 @@ k_stage_nhwc_flat(const uint8_t* __restrict__ src, const int64_t* __restrict__ r
                     w[c][0] = q.x; w[c][1] = q.y;
                 }
             }
-            constexpr int per = 16 / (int)sizeof(TO);
+            constexpr int per = 16 / (int)sizeof(TO);     // outputs per 16-byte smem store
             uint4* d16 = reinterpret_cast<uint4*>(o + (size_t)q0 * C);
 #pragma unroll
-            for (int v = 0; v < PX * C / per; ++v) {
-                TO e[per];
-#pragma unroll
-                for (int j = 0; j < per; ++j) {
-                    const int k = v * per + j, px = k / C, c = k % C;
-                    e[j] = Out<OUT>::cvt((float)((w[c][px >> 2] >> ((px & 3) * 8)) & 0xFFu));
-                }
-                uint4 q;
-                memcpy(&q, e, 16);
-                d16[v] = q;
-            }
+            for (int v = 0; v < PX * C / per; ++v) d16[v] = u8_nhwc_vec16<OUT, C, PX / 4>(w, v);
         } else {
             for (int q = q0; q < npx && q < q0 + PX; ++q)
                 for (int c = 0; c < C; ++c) o[q * C + c] = Out<OUT>::cvt((float)pl[c * TP + q]);

@@ -92,6 +92,8 @@ n = x.shape[0]
 E = x[0].numel()
 out["k2_stage_u8_bf16_nhwc"] = timeit(lambda: stage_rows(x, torch.uint8, tuple(x.shape[1:]), None, 0, n,
                                                          Staging(torch.bfloat16, True), dev), n * E * 3)
+out["k2_stage_u8_f32_nhwc"] = timeit(lambda: stage_rows(x, torch.uint8, tuple(x.shape[1:]), None, 0, n,
+                                                        Staging(torch.float32, True), dev), n * E * 5)
 out["k2_stage_u8_f32_nchw"] = timeit(lambda: stage_rows(x, torch.uint8, tuple(x.shape[1:]), None, 0, n,
                                                         Staging(torch.float32, False), dev), n * E * 5)
 xf = torch.randn((n,) + w.sample_shape, device=dev)
