@@ -556,7 +556,8 @@ def run_gpu(args, w, ws, rank, local):
                    "l2": "inputs > L2: every mini-batch is %.1f GB of uint8, none reused within a step"
                          % (n_b * int(np.prod(w.sample_shape)) / 1e9),
                    "api": ("engine.train_epoch" if ws == 1 else "dp.DataParallelMBS.train_epoch (per-rank shards, "
-                           "one all-reduce per global mini-batch, transport=%s)" % dp.transport)})
+                           "one all-reduce per global mini-batch, transport=%s over the %s process group)"
+                           % (dp.transport, torch.distributed.get_backend()))})
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",

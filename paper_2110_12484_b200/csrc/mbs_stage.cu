@@ -571,7 +571,8 @@ static int launch_flat(const uint8_t* s, const int64_t* rows, int64_t row0, int6
         if (per_sm < 1) per_sm = 1;
     }
     const int64_t total = n_rows * HW;
-    const int64_t resident = (int64_t)sm_count() * per_sm;
+    static const int cap = getenv("MBS_K2_CTAS_PER_SM") ? atoi(getenv("MBS_K2_CTAS_PER_SM")) : 0;  // A/B only
+    const int64_t resident = (int64_t)sm_count() * (cap > 0 ? std::min(cap, per_sm) : per_sm);
     int64_t per_cta = (total + resident - 1) / resident;
     per_cta = std::max<int64_t>(16, (per_cta + 15) / 16 * 16);   // 16-byte aligned bulk copies
     const int grid = (int)((total + per_cta - 1) / per_cta);

@@ -82,6 +82,24 @@ acc.begin(1 << 15)
 acc.add_tensors(grads, 0.125)
 out["k1_accumulate"] = timeit(k1_accum, 12 * P)
 out["k1_accumulate_norm"] = timeit(k1_last, 12 * P)
+# shadow-weight mode (the bench): bf16 gradients for the conv / linear weights, fp32 for BN and biases
+gmix = [g.to(torch.bfloat16) if g.dim() >= 2 else g for g in grads]
+nb_g = sum(g.numel() * g.element_size() for g in gmix)
+
+
+def k1m_assign():
+    acc.begin(1 << 15)
+    acc.add_tensors(gmix, 0.125)
+
+
+acc.begin(1 << 15)
+acc.add_tensors(gmix, 0.125)
+out["k1_assign_bf16g"] = timeit(k1m_assign, nb_g + 4 * P)
+acc.begin(1 << 15)
+acc.add_tensors(gmix, 0.125)
+out["k1_accumulate_bf16g"] = timeit(lambda: acc.add_tensors(gmix, 0.125), nb_g + 8 * P)
+acc.begin(1 << 15)
+acc.add_tensors(grads, 0.125)
 gs = acc.as_gradient_set()
 st = mbs.sgd_state(0.01, 0.9, 5e-4)
 out["k3_sgd"] = timeit(lambda: mbs.apply_update(params, gs, st), 20 * P)
