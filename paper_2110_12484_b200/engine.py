@@ -155,6 +155,7 @@ class GradientAccumulator:
         self._k1_bytes_acc = self._k1_bytes_assign + 4 * self.layout.n_params
         self._pending_zero = False
         self._fresh = True
+        self._norm_valid = False
         self._covered = 0
         self.expected = expected
         if expected is not None:
@@ -189,6 +190,7 @@ class GradientAccumulator:
         self.expected = expected
         self._pending_zero = True
         self._fresh = True
+        self._norm_valid = False
         self._covered = 0
 
     def add(self, grads: GradientSet | dict) -> None:
@@ -208,7 +210,10 @@ class GradientAccumulator:
     def as_gradient_set(self) -> GradientSet:
         """engine.py:130-131 — a GradientSet ALIASING the live sums."""
         self._materialize()
-        return GradientSet(dict(self._views), flat=self.flat, layout=self.layout, norm2=self.stats_dev[0])
+        # the device norm is attached only when finalize() reduced it for exactly these sums; otherwise
+        # GradientSet.l2_norm() recomputes it and the K3 guard is off (the reference has no guard)
+        norm2 = self.stats_dev[0] if self._norm_valid else None
+        return GradientSet(dict(self._views), flat=self.flat, layout=self.layout, norm2=norm2)
 
     # -- B200 surface --
     def _materialize(self):
@@ -271,6 +276,7 @@ class GradientAccumulator:
             nb = sum((2 if t.dtype == torch.bfloat16 else 4) * t.numel() for t in keep[:n])
             elems = sum(self.layout.numels[seg_begin:seg_begin + n])
             TIMER.stop("k1_accumulate", t0, nb + (4 if self._fresh else 8) * elems, stream)
+        self._norm_valid = False   # a K1 pass since the last finalize
         self._covered += n
         if self._covered >= len(self.layout.names):
             self._covered = 0
@@ -300,6 +306,7 @@ class GradientAccumulator:
         if t0 is not None:
             TIMER.stop("k1_accumulate", t0, self._k1_bytes_assign if self._fresh else self._k1_bytes_acc, stream)
         self._fresh = False
+        self._norm_valid = False   # a K1 pass since the last finalize
         self._covered = 0
         self._pending_zero = False
 
@@ -341,6 +348,7 @@ class GradientAccumulator:
         if t0 is not None:
             TIMER.stop("k1_accumulate", t0, self._k1_bytes_assign if self._fresh else self._k1_bytes_acc, stream)
         self._fresh = False
+        self._norm_valid = False   # a K1 pass since the last finalize
         self._covered = 0
         self._pending_zero = False
         for p in self._plist:
@@ -377,6 +385,7 @@ class GradientAccumulator:
                                                 float(timeout_ms), _stream_ptr(stream)), "mbs_accum_add_allreduce")
         TIMER.stop("k1c_accumulate_allreduce", t0, 12 * self.layout.n_params, stream)
         self._fresh = False
+        self._norm_valid = False   # a K1 pass since the last finalize
         self._covered = 0
         self._pending_zero = False
         if from_module:
@@ -393,6 +402,7 @@ class GradientAccumulator:
         N.check(N.lib().mbs_accum_finalize(self._h, int(n_b), self.stats_dev.data_ptr(), _stream_ptr(stream)),
                 "mbs_accum_finalize")
         TIMER.stop("k4_finalize", t0, 0, stream)
+        self._norm_valid = True
         return self.stats_dev
 
 

@@ -168,3 +168,25 @@ def test_size1_dim_strides_are_not_copied(cuda):
     assert torch.equal(acc.sums[w], g)
     assert not acc._same_memory_order(torch.randn(256, 64, 1, 1, device=cuda).transpose(0, 1).reshape(
         256, 64, 1, 1)[:, :, :, :].as_strided((256, 64, 1, 1), (1, 256, 1, 1)), 0)
+
+
+def test_gradient_set_norm_is_never_stale(cuda):
+    """The device norm is attached to as_gradient_set() only when finalize() reduced it for the current
+    sums; a later reference-style begin/add (engine.py:110-131) gets a freshly computed l2_norm."""
+    bag, params = _setup(cuda)
+    acc = mbs.GradientAccumulator(params)
+    acc.begin(1)
+    g1 = [torch.randn(s, device=cuda) for s in params.layout.shapes]
+    acc.add_tensors(g1, 1.0, loss=torch.ones((), device=cuda), loss_weight=1.0, last=True)
+    acc.finalize(1)
+    gs = acc.as_gradient_set()
+    assert gs.norm2 is not None
+    want1 = float(torch.sqrt(sum((t.double() ** 2).sum() for t in g1)))
+    assert gs.l2_norm() == pytest.approx(want1, rel=1e-6)
+    acc.begin(1)
+    g2 = {n: 3.0 * torch.randn(s, device=cuda) for n, s in zip(params.names(), params.layout.shapes)}
+    acc.add(g2)
+    gs2 = acc.as_gradient_set()
+    assert gs2.norm2 is None
+    want2 = float(torch.sqrt(sum((t.double() ** 2).sum() for t in g2.values())))
+    assert gs2.l2_norm() == pytest.approx(want2, rel=1e-6)
