@@ -57,9 +57,6 @@ constexpr int kUnroll = MBS_K1_UNROLL;
 #ifndef MBS_K1_BF16_X4
 #define MBS_K1_BF16_X4 1
 #endif
-#ifndef MBS_K1_ASSIGN_U
-#define MBS_K1_ASSIGN_U 8
-#endif
 
 struct Seg {
     int64_t off;   // element offset of the segment in acc (multiple of 4)
@@ -223,38 +220,12 @@ __device__ __forceinline__ void accum_piece(float* __restrict__ a, const G* __re
             }
             done = n8 << 3;
         } else if ((reinterpret_cast<uintptr_t>(g) & 7) == 0) {
-            // 8-byte bf16x4 loads, U of them in flight per thread before the first store. The first
-            // micro-batch's assign pass reads no accumulator, so it takes a deeper unroll to keep as many
-            // bytes in flight (ncu r02: at the compiler's 4-deep unroll it ran at 0.80 of the copy peak,
-            // 0.36 eligible warps per scheduler, scoreboard-bound).
-            constexpr int U = ASSIGN ? MBS_K1_ASSIGN_U : 4;
             const int n4 = n >> 2;
-            const uint2* g2 = reinterpret_cast<const uint2*>(g);
-            for (int base = threadIdx.x; base < n4; base += kThreads * U) {
-                uint2 gr[U];
-                float4 av[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int i = base + u * kThreads;
-                    if (i < n4) {
-                        asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
-                                     : "=r"(gr[u].x), "=r"(gr[u].y) : "l"(g2 + i));
-                        if (!ASSIGN) av[u] = ld_acc(a4 + i);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int i = base + u * kThreads;
-                    if (i < n4) {
-                        const float4 gv = make_float4(__uint_as_float(gr[u].x << 16),
-                                                      __uint_as_float(gr[u].x & 0xffff0000u),
-                                                      __uint_as_float(gr[u].y << 16),
-                                                      __uint_as_float(gr[u].y & 0xffff0000u));
-                        const float4 r = axpy4<ASSIGN>(s, gv, av[u]);
-                        a4[i] = r;
-                        if (NORM) sq += sq4(r);
-                    }
-                }
+            for (int i = threadIdx.x; i < n4; i += kThreads) {
+                const float4 gv = ld_stream_bf16x4(reinterpret_cast<const uint2*>(g) + i);
+                const float4 r = axpy4<ASSIGN>(s, gv, ASSIGN ? gv : ld_acc(a4 + i));
+                a4[i] = r;
+                if (NORM) sq += sq4(r);
             }
             done = n4 << 2;
         }
