@@ -161,18 +161,20 @@ class SharedHostPool:
             os.unlink(self.path)
 
 
-def workload_config(w, n_b: int, n_mu: int, ws: int, model_ops: str) -> dict:
-    """The ``config`` object of BOTH arms' JSON lines (the workload; what a sample of it ran is separate)."""
+def workload_config(w, n_b: int, n_mu: int, ws: int) -> dict:
+    """The ``config`` object of BOTH arms' JSON lines: the workload only (identical in the two arms, so the
+    driver can compare them); how each arm ran it is in the line's ``setup``."""
     from paper_2110_12484_b200 import engine
     plan = engine.plan_split(n_b, n_mu)
     row = int(np.prod(w.sample_shape))
-    return {"workload": w.name, "model": w.model, "input": "x".join(map(str, w.sample_shape)),
+    return {"workload": w.name, "input": "x".join(map(str, w.sample_shape)),
             "mini_batch_per_gpu": n_b, "micro_batch": n_mu, "n_micro": plan.n_s_mu,
             "micro_sizes_head_tail": [plan.sizes[0], plan.sizes[-1]], "global_batch": n_b * ws,
             "parallelism": f"dp{ws}", "normalization": w.normalization, "optimizer": w.optimizer,
             "loss": w.loss_kind,
             "mini_batch_bytes": {"uint8": n_b * row, "fp32_as_reference_holds_it": 4 * n_b * row},
-            "model_ops": model_ops}
+            "l2": "inputs > L2: every mini-batch is %.1f GB of uint8, none reused within a step" % (n_b * row / 1e9)
+            if n_b * row > (126 << 20) else "mini-batch fits L2 (no flush): CPU-sized config"}
 
 
 # ---------------------------------------------------------------------------
@@ -237,7 +239,9 @@ def reference_arm(args, w, ws, rank):
     line = {"impl": "reference", "metric": METRIC, "value": sps, "unit": "samples/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(w, w.mini, w.micro or 128, ws, "reference numerics (float64 CPU)"),
+            "config": workload_config(w, w.mini, w.micro or 128, ws),
+            "setup": {"model": w.model, "model_ops": "reference numerics (float64 CPU, oracle port)",
+                      "api": "oracle.mbs_oracle.train_mini_batch (engine.py:233-261 restated)"},
             "reference_sample": {"mini_batch": n_b, "micro_batch": n_mu, "steps": args.steps,
                                  "warmup": args.warmup},
             "cpu_baseline": {"value": sps, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
@@ -550,10 +554,12 @@ def run_gpu(args, w, ws, rank, local):
         _graphs.clear()
         fp32_ctx = fp32_context(w, dev, n_mu, warm_small, args.model_ops, x_dev, y_dev)
 
-    config = workload_config(w, n_b, n_mu, ws, "BatchNorm(+ReLU/+skip add) on K5, max-pool (+U-Net skip join) on K6, "
-                             "stem conv as K7 im2col + GEMM, micro-batch statistics; micro step replayed from "
-                             "CUDA graphs" if args.model_ops == "native" else "stock torch")
-    config.update({"precision": precision["detail"], "autosize": autosize,
+    config = workload_config(w, n_b, n_mu, ws)
+    setup = {"model": w.model,
+             "model_ops": "BatchNorm(+ReLU/+skip add) on K5, max-pool (+U-Net skip join) on K6, stem conv as K7 "
+                          "im2col + GEMM, micro-batch statistics; micro step replayed from CUDA graphs"
+                          if args.model_ops == "native" else "stock torch"}
+    setup.update({"precision": precision["detail"], "autosize": autosize,
                    "host_dataset": {"mini_batches": d_minis, "samples": d_minis * n_b,
                                     "bytes": int(x_host.numel() * x_host.element_size() +
                                                  y_host.numel() * y_host.element_size()),
@@ -565,8 +571,6 @@ def run_gpu(args, w, ws, rank, local):
                                 f"{d_minis} steps, reshuffled by epoch_index",
                    "warmup_is": f"{args.warmup} full mini-batches before the HBM-resident (value) run; 1 mini-batch "
                                 f"of {warm_small} through the host streamer before the e2e run",
-                   "l2": "inputs > L2: every mini-batch is %.1f GB of uint8, none reused within a step"
-                         % (n_b * int(np.prod(w.sample_shape)) / 1e9),
                    "api": ("engine.train_epoch" if ws == 1 else "dp.DataParallelMBS.train_epoch (per-rank shards, "
                            "one all-reduce per global mini-batch, transport=%s over the %s process group)"
                            % (dp.transport, torch.distributed.get_backend()))})
@@ -574,7 +578,7 @@ def run_gpu(args, w, ws, rank, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (uint8 images, random labels / masks; random-init weights)",
-            "config": config,
+            "config": config, "setup": setup,
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": int(h2d_bytes),
                     "d2h_bytes_per_step": 8 * (4 + 2 * plan.n_s_mu), "ms_per_step": ms_host / args.steps,
                     "wall_s": wall_host},
