@@ -186,7 +186,10 @@ class MicroMaxPool2d(nn.MaxPool2d):
     """``nn.MaxPool2d`` whose CUDA forward/backward run K6 (bit-identical to torch)."""
 
     def forward(self, x, dual: bool = False):
-        if not x.is_cuda or x.dim() != 4:
+        if not x.is_cuda and self.training:
+            raise RuntimeError("MicroMaxPool2d: training runs on the sm_100a K6 kernels (libmbs_native.so) and "
+                               "needs a CUDA tensor; there is no CPU fallback")
+        if not x.is_cuda or x.dim() != 4:           # eval-mode inference of a CPU copy / unbatched input
             y = super().forward(x)
             return (y, y) if dual else y
         return _MaxPoolFn.apply(x, self._k, self._s, self._p, dual)

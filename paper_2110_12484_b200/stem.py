@@ -89,7 +89,10 @@ class StemConv2d(nn.Conv2d):
 
     def forward(self, x):
         if not x.is_cuda:
-            return super().forward(x)
+            if self.training:
+                raise RuntimeError("StemConv2d: training runs on the sm_100a K7 kernel (libmbs_native.so) and "
+                                   "needs a CUDA tensor; there is no CPU fallback")
+            return super().forward(x)          # eval-mode inference of a CPU copy: the same convolution
         return _StemConvFn.apply(x, self.weight, self.bias, self._k, self._s, self._p)
 
 

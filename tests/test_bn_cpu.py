@@ -60,7 +60,22 @@ def test_swap_maxpool_supported_configs():
     kinds = [type(x).__name__ for x in m]
     assert kinds == ["MicroMaxPool2d", "MicroMaxPool2d", "MaxPool2d", "MaxPool2d", "MaxPool2d"]
     x = torch.randn(2, 4, 9, 9)
-    torch.testing.assert_close(m[0](x), torch.nn.functional.max_pool2d(x, 3, 2, 1))   # CPU: torch path
+    with pytest.raises(RuntimeError, match="no CPU fallback"):                       # training: K6 only
+        m[0](x)
+    m.eval()
+    torch.testing.assert_close(m[0](x), torch.nn.functional.max_pool2d(x, 3, 2, 1))   # CPU eval: torch path
+
+
+def test_stem_training_on_cpu_fails_loudly():
+    from paper_2110_12484_b200 import stem as K7
+    m = K7.swap_stem(torch.nn.Sequential(torch.nn.Conv2d(3, 8, 7, 2, 3)))
+    assert type(m[0]).__name__ == "StemConv2d"
+    x = torch.randn(2, 3, 16, 16)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        m(x)
+    m.eval()
+    ref = torch.nn.functional.conv2d(x, m[0].weight, m[0].bias, 2, 3)
+    torch.testing.assert_close(m(x), ref)
 
 
 def test_build_model_native_ops():
