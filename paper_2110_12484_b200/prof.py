@@ -3,8 +3,11 @@
 When enabled, every K1 / K2 / K3 launch made through the package is bracketed
 by a pair of timing events recorded on the stream it is launched on, together
 with its ALGORITHMIC byte count (what the reference semantics must move:
-K1 12 B/param for acc += s*g, 8 B/param for the first micro-batch's
-acc = s*g; K3 20 B/param SGD, 28 B/param Adam; K2 source + staged bytes).
+K1 (g bytes + 8) B/param for acc += s*g and (g bytes + 4) B/param for the
+first micro-batch's acc = s*g — g is 4 B fp32, or 2 B for the bf16 weight
+gradients of shadow-weight mode, so 12/8 or 10/6 B/param; K3 20 B/param SGD,
+28 B/param Adam, +2 B/param when it also writes the bf16 shadow; K2 source +
+staged bytes).
 Disabled (the default) it costs one attribute test per launch.
 """
 
