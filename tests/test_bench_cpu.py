@@ -24,3 +24,22 @@ def test_reference_arm_json_line():
     assert line["config"]["mini_batch_per_gpu"] == 64 and line["config"]["micro_batch"] == 8
     assert line["reference_sample"] == {"mini_batch": 16, "micro_batch": 8, "steps": 1, "warmup": 3}
     assert line["warmup"] == 3 and line["steps"] == 1
+
+
+def test_reference_arm_under_torchrun_prints_one_line():
+    """N>1 launch of the reference arm (as the driver does it): rank 0 alone runs and prints; the others exit 0."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--impl", "reference", "--gpus", "2", "--config", "c1", "--steps", "1", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["config"]["parallelism"] == "dp2" and line["config"]["global_batch"] == 128
