@@ -254,7 +254,12 @@ int mbs_accum_add_allreduce(mbs_accum_t h, mbs_peer_t peer, const float* const* 
  * ------------------------------------------------------------------------- */
 int mbs_bn_workspace_bytes(int64_t rows, int64_t C, int dtype, int64_t* bytes);
 /* num_batches_tracked (nullable, device int64): incremented by one on the stream (torch's
- * BatchNorm2d.num_batches_tracked += 1), so no separate counter kernel runs per layer. */
+ * BatchNorm2d.num_batches_tracked += 1), so no separate counter kernel runs per layer.
+ * `relu` is a flag word: MBS_BN_RELU fuses the ReLU; MBS_BN_BIASED_RUNNING_VAR makes the running-variance
+ * update take the biased micro-batch variance, as the reference does (nn.py:329-332), instead of torch's
+ * unbiased one. */
+#define MBS_BN_RELU 1
+#define MBS_BN_BIASED_RUNNING_VAR 2
 int mbs_bn_forward(const void* x, const void* residual, void* y, int dtype, int64_t rows, int64_t C,
                    const float* weight, const float* bias, float* running_mean, float* running_var,
                    int64_t* num_batches_tracked, double momentum, double eps, int relu, float* save_mean,
@@ -262,7 +267,8 @@ int mbs_bn_forward(const void* x, const void* residual, void* y, int dtype, int6
 /* Gradients of mbs_bn_forward: dx, dresidual (iff residual), dweight/dbias (may be NULL).
  * The ReLU mask is recomputed from x (and residual) bit-identically to the forward.
  * dy2 (nullable): a second gradient of y (the output feeds both the next block's main path and its
- * skip), summed with dy in fp32 inside the kernel; only with residual + relu, C/8 (bf16) or C/4 (fp32)
+ * skip), summed with dy inside the kernel and rounded to the activation dtype exactly like torch's add;
+ * only with residual + relu, C/8 (bf16) or C/4 (fp32)
  * vectors <= 256 and every pointer 16-byte aligned — otherwise MBS_ERR_INVALID. */
 int mbs_bn_backward(const void* x, const void* residual, const void* dy, const void* dy2, void* dx,
                     void* dresidual, int dtype, int64_t rows, int64_t C, const float* weight, const float* bias,
@@ -284,7 +290,8 @@ int mbs_maxpool_forward(const void* x, void* y, uint8_t* idx, int dtype, int64_t
                         int k, int s, int p, void* stash, int64_t stash_C, int64_t stash_c0, void* stream);
 /* addend (nullable): dx += addend[..., add_c0:add_c0+C] (channels-last, add_C channels), summed in
  * fp32 before dx's single rounding (the skip-connection gradient, fused).
- * dy2 (nullable): a second gradient of y (y has two consumers), added to dy in fp32 per window. */
+ * dy2 (nullable): a second gradient of y (y has two consumers), added to dy per window and rounded to the
+ * activation dtype like torch's add. */
 int mbs_maxpool_backward(const void* dy, const void* dy2, const uint8_t* idx, void* dx, int dtype, int64_t N,
                          int64_t H, int64_t W, int64_t C, int k, int s, int p, const void* addend, int64_t add_C,
                          int64_t add_c0, void* stream);

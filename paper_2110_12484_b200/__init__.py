@@ -9,7 +9,7 @@ model's micro-batch BatchNorm (+ReLU/+skip add) when a model is passed through
 ``bn.fuse_batchnorm``.
 """
 
-from . import _native, bn, pool, stem
+from . import _native, bn, pool, refspec, stem
 from .engine import (NORMALIZATION_MODES, EpochStats, GradientAccumulator, MicroBatchPlan, MiniBatchStats,
                      accumulate, make_streamer, mini_batch_gradient, normalization_factor, normalize_loss,
                      plan_split, train_epoch, train_mini_batch)

@@ -123,7 +123,7 @@ class _MicroBatchNormFn(torch.autograd.Function):
         # algorithmic bytes: stats read x; apply read x (+ residual), write y
         TIMER.stop("k5_bn_forward", ev, x.numel() * x.element_size() * (3 + (residual is not None)), stream)
         ctx.save_for_backward(x, residual, weight, bias, mean, invstd)
-        ctx.relu = bool(relu)
+        ctx.relu = bool(int(relu) & 1)          # relu is the C-ABI flag word (bit 1: biased running variance)
         ctx.code = code
         ctx.has_res = residual is not None
         if dual:
@@ -165,12 +165,15 @@ class _MicroBatchNormFn(torch.autograd.Function):
 
 
 def micro_batch_norm(x, weight, bias, running_mean=None, running_var=None, *, momentum=0.1, eps=1e-5,
-                     relu=False, residual=None, dual=False):
+                     relu=False, residual=None, dual=False, biased_running_var=False):
     """Functional form: ``relu?(batch_norm(x, training=True) [+ residual])`` on the native kernels
-    (``dual``: the output as two autograd handles, see ``MicroBatchNorm2d.forward``)."""
+    (``dual``: the output as two autograd handles, see ``MicroBatchNorm2d.forward``;
+    ``biased_running_var``: the running variance takes the biased micro-batch variance, the reference's
+    convention, nn.py:329-332, instead of torch's unbiased one)."""
     if residual is not None and not relu:
         raise ValueError("a residual is only fused together with the ReLU")
-    return _MicroBatchNormFn.apply(x, residual, weight, bias, running_mean, running_var, momentum, eps, relu, dual)
+    flags = (1 if relu else 0) | (2 if biased_running_var else 0)
+    return _MicroBatchNormFn.apply(x, residual, weight, bias, running_mean, running_var, momentum, eps, flags, dual)
 
 
 class MicroBatchNorm2d(nn.BatchNorm2d):

@@ -95,6 +95,7 @@ struct BnGeom {
     int64_t chunk;     // rows per CTA
     int P;             // CTAs along rows (= partials per channel for the reductions)
     long long* nbt = nullptr;   // num_batches_tracked, incremented once by the statistics finalize (nullable)
+    bool biased_rv = false;     // running_var takes the biased variance (the reference, nn.py:329-332)
 };
 
 // Per-channel affine of the forward (shared by forward apply and the backward mask
@@ -296,7 +297,7 @@ __device__ __forceinline__ void bn_stats_write(const T* __restrict__ x, const Bn
     save_invstd[c] = (float)(1.0 / sqrt(var + eps));
     if (running_mean) {
         running_mean[c] = (float)((1.0 - momentum) * (double)running_mean[c] + momentum * mean);
-        const double unbiased = g.rows > 1 ? var * m / (m - 1.0) : var;
+        const double unbiased = (g.rows > 1 && !g.biased_rv) ? var * m / (m - 1.0) : var;
         running_var[c] = (float)((1.0 - momentum) * (double)running_var[c] + momentum * unbiased);
     }
     float sc, mu, be;
@@ -984,7 +985,7 @@ static cudaError_t fused_bwd(const T* X, const T* DY, const T* R, T* DX, T* DR, 
 template <typename T, int V>
 static int bn_forward_t(const void* x, const void* res, void* y, int64_t rows, int64_t C, const float* w,
                         const float* b, float* rm, float* rv, long long* nbt, double momentum, double eps, int relu,
-                        float* smean, float* sinv, void* ws, cudaStream_t s) {
+                        float* smean, float* sinv, void* ws, cudaStream_t s, bool biased_rv) {
     const T* X = static_cast<const T*>(x);
     const T* R = static_cast<const T*>(res);
     T* Y = static_cast<T*>(y);
@@ -993,6 +994,7 @@ static int bn_forward_t(const void* x, const void* res, void* y, int64_t rows, i
     BnGeom g;
     g.rows = rows;
     g.C = C;
+    g.biased_rv = biased_rv;
     const bool tma = tma_ok(C, V);
     if (tma && fused_mode() && rows * C * (int64_t)sizeof(T) <= fused_max_bytes()) {
         cudaError_t e;
@@ -1127,6 +1129,9 @@ int mbs_bn_forward(const void* x, const void* residual, void* y, int dtype, int6
                    float* save_invstd, void* workspace, void* stream) {
     if (!x || !y || !save_mean || !save_invstd || !workspace) return invalid("mbs_bn_forward: null pointer");
     if (rows < 1 || C < 1) return invalid("mbs_bn_forward: rows and C must be >= 1");
+    if (relu & ~(MBS_BN_RELU | MBS_BN_BIASED_RUNNING_VAR)) return invalid("mbs_bn_forward: unknown flag bits");
+    const bool biased_rv = (relu & MBS_BN_BIASED_RUNNING_VAR) != 0;
+    relu &= MBS_BN_RELU;
     if (!!running_mean != !!running_var) return invalid("mbs_bn_forward: running_mean/running_var must both be set");
     if (residual && !relu) return invalid("mbs_bn_forward: a residual is only fused together with the ReLU");
     if (!(eps > 0.0)) return invalid("mbs_bn_forward: eps must be > 0");
@@ -1136,14 +1141,14 @@ int mbs_bn_forward(const void* x, const void* residual, void* y, int dtype, int6
     const int V = dtype == MBS_BF16 || dtype == MBS_F32 ? bn_vec(dtype, C, ptrs, 3) : 0;
     if (dtype == MBS_BF16)
         return V == 8 ? bn_forward_t<__nv_bfloat16, 8>(x, residual, y, rows, C, weight, bias, running_mean, running_var,
-                                                       nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s)
+                                                       nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s, biased_rv)
                       : bn_forward_t<__nv_bfloat16, 1>(x, residual, y, rows, C, weight, bias, running_mean, running_var,
-                                                       nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s);
+                                                       nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s, biased_rv);
     if (dtype == MBS_F32)
         return V == 4 ? bn_forward_t<float, 4>(x, residual, y, rows, C, weight, bias, running_mean, running_var,
-                                               nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s)
+                                               nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s, biased_rv)
                       : bn_forward_t<float, 1>(x, residual, y, rows, C, weight, bias, running_mean, running_var,
-                                               nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s);
+                                               nbt, momentum, eps, relu, save_mean, save_invstd, workspace, s, biased_rv);
     return invalid("mbs_bn_forward: dtype must be MBS_BF16 or MBS_F32");
 }
 
