@@ -807,8 +807,10 @@ static cudaError_t launch_reduce(const T* X, const T* DY, const T* R, const floa
     // statistics: at most 32 channel vectors per CTA (A/B: profiles/r01_k5_stats_gv_ab.txt), so wide layers (C = 1024 / 2048 on few rows) are
     // split into channel groups instead of into hundreds of row chunks — their per-CTA partials
     // (8 B per channel) were ~25 % of the input bytes
+    const bool biased_rv = g.biased_rv;      // the geometry is recomputed; the update convention is kept
     g = bn_geom(g.rows, g.C, V, MODE == 0 ? 16 : 32, std::min(wave_ctas(k), kMaxReduceCtas),
                 MODE == 0 ? stats_max_gv() : kBnThreads);
+    g.biased_rv = biased_rv;
     return launch_pdl(k, dim3(g.P, (unsigned)bn_groups(g, V)), s, X, DY, R, w, b, mean, invstd, part, g);
 }
 
@@ -932,7 +934,9 @@ template <typename K>
 static bool coop_geometry(K kernel, BnGeom& g, int V) {
     const CoopInfo info = coop_info(kernel);
     if (info.resident < 1) return false;
+    const bool biased_rv = g.biased_rv;      // the geometry is recomputed; the update convention is kept
     g = bn_geom(g.rows, g.C, V, 16, std::min(info.resident, kMaxReduceCtas));
+    g.biased_rv = biased_rv;
     return true;
 }
 
