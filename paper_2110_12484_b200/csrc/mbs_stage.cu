@@ -427,12 +427,12 @@ constexpr size_t flat_smem_bytes() {
     return (size_t)kFlatStages * C * TP + 2 * (size_t)TP * C * sizeof(TO);
 }
 
-template <int OUT, int C, int TP>
-__global__ void __launch_bounds__(kStageThreads)
+template <int OUT, int C, int TP, int NT = kStageThreads>
+__global__ void __launch_bounds__(NT)
 k_stage_nhwc_flat(const uint8_t* __restrict__ src, const int64_t* __restrict__ rows, int64_t row0, int64_t HW,
                   int64_t total_px, int64_t per_cta, typename Out<OUT>::T* __restrict__ dst) {
     using TO = typename Out<OUT>::T;
-    constexpr int PX = TP / kStageThreads;
+    constexpr int PX = TP / NT;
     static_assert(PX == 8 || PX == 16, "tile must give 8 or 16 pixels per thread");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full[kFlatStages];
@@ -515,6 +515,11 @@ static int stage_path() {
     return e ? atoi(e) : 4;
 }
 
+static bool flat_small() {   // A/B only: MBS_K2_FLAT=128 -> 128-thread CTAs on 1024-pixel tiles (more CTAs per SM)
+    const char* e = getenv("MBS_K2_FLAT");
+    return e && atoi(e) == 128;
+}
+
 static int bulk_tile() {
     const char* e = getenv("MBS_K2_TILE");   // A/B only: 2048 (default) or 4096 pixels per tile
     return (e && atoi(e) == 4096) ? 4096 : 2048;
@@ -558,16 +563,16 @@ static int launch_bulk(const uint8_t* s, const int64_t* rows, int64_t row0, int6
     return MBS_OK;
 }
 
-template <int OUT, int C, int TP>
+template <int OUT, int C, int TP, int NT = kStageThreads>
 static int launch_flat(const uint8_t* s, const int64_t* rows, int64_t row0, int64_t n_rows, int64_t HW,
                        typename Out<OUT>::T* d, cudaStream_t st) {
     using TO = typename Out<OUT>::T;
-    auto kern = k_stage_nhwc_flat<OUT, C, TP>;
+    auto kern = k_stage_nhwc_flat<OUT, C, TP, NT>;
     constexpr size_t sm = flat_smem_bytes<TP, C, TO>();
     static int per_sm = 0;
     if (!per_sm) {
         MBS_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        MBS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStageThreads, sm));
+        MBS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
         if (per_sm < 1) per_sm = 1;
     }
     const int64_t total = n_rows * HW;
@@ -576,7 +581,7 @@ static int launch_flat(const uint8_t* s, const int64_t* rows, int64_t row0, int6
     int64_t per_cta = (total + resident - 1) / resident;
     per_cta = std::max<int64_t>(16, (per_cta + 15) / 16 * 16);   // 16-byte aligned bulk copies
     const int grid = (int)((total + per_cta - 1) / per_cta);
-    kern<<<grid, kStageThreads, sm, st>>>(s, rows, row0, HW, total, per_cta, d);
+    kern<<<grid, NT, sm, st>>>(s, rows, row0, HW, total, per_cta, d);
     MBS_CK_LAUNCH("k_stage_nhwc_flat");
     return MBS_OK;
 }
@@ -635,7 +640,8 @@ static int stage_typed(const void* src, const int64_t* rows, int64_t row0, int64
                 is_device_memory(src)) {
                 switch (C) {
                     case 2: return launch_flat<OUT, 2, 2048>(s, rows, row0, n_rows, HW, d, st);
-                    case 3: return launch_flat<OUT, 3, 2048>(s, rows, row0, n_rows, HW, d, st);
+                    case 3: return flat_small() ? launch_flat<OUT, 3, 1024, 128>(s, rows, row0, n_rows, HW, d, st)
+                                                : launch_flat<OUT, 3, 2048>(s, rows, row0, n_rows, HW, d, st);
                     default: return launch_flat<OUT, 4, 2048>(s, rows, row0, n_rows, HW, d, st);
                 }
             }

@@ -56,7 +56,7 @@ def test_stage_bit_exact(cuda, src_dtype, dst_dtype, shape, cl):
     assert torch.equal(_bits(got2), _bits(want2))
 
 
-@pytest.mark.parametrize("path", ["0", "1", "2", "3", "3:2048", "4"])
+@pytest.mark.parametrize("path", ["0", "1", "2", "3", "3:2048", "4", "4:flat128"])
 @pytest.mark.parametrize("dst_dtype", [torch.float32, torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("shape", [(9, 3, 80, 80), (5, 3, 224, 224), (7, 4, 64, 64), (6, 2, 48, 48),
                                    (300, 3, 16, 16)])
@@ -67,6 +67,7 @@ def test_stage_u8_nhwc_every_path(cuda, monkeypatch, path, dst_dtype, shape):
     more tiles than resident CTAs."""
     monkeypatch.setenv("MBS_K2_PATH", path.split(":")[0])
     monkeypatch.setenv("MBS_K2_TILE", path.split(":")[-1])
+    monkeypatch.setenv("MBS_K2_FLAT", "128" if path.endswith("flat128") else "0")
     x = _src(torch.uint8, shape, cuda)
     rows = torch.from_numpy(O.epoch_order(shape[0], 5, 2).astype(np.int64)).to(cuda)
     st = Staging(dtype=dst_dtype, channels_last=True)
