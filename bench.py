@@ -462,7 +462,9 @@ def run_gpu(args, w, ws, rank, local):
         r = None
         while b >= 1 and r is None:
             try:
-                r = no_stream_baseline(w, dev, b, args.steps, args.warmup, ws, ops=ops_)
+                with ClockSampler(dev.index) as ck:
+                    r = no_stream_baseline(w, dev, b, args.steps, args.warmup, ws, ops=ops_)
+                r["clocks"] = ck.summary()
             except torch.OutOfMemoryError:
                 b //= 2
             torch.cuda.empty_cache()
@@ -685,14 +687,19 @@ def fp32_context(w, dev, n_mu, mini, model_ops, x_dev, y_dev):
         torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32 = tf
 
 
-def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True):
+NO_STREAM_MIN_S = 30.0          # the no-stream baseline runs at least this long (same power / clock state as MBS)
+
+
+def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True, min_s=NO_STREAM_MIN_S):
     """The paper's 'w/o MBS' run: plain torch training, batch = micro-batch, data resident in HBM.
 
     ``ops`` selects the same model definition as the MBS run (native K5/K6/K7 or stock torch ops).
     ``graph``: the whole training step (fwd + bwd + fused optimizer step) is replayed from one CUDA
     graph, like the MBS micro step — eager, this loop is host-bound on B200 and its number then
     tracks the host CPU rather than the GPU. Falls back to eager if capture fails. Every step is
-    bracketed by CUDA events (the baseline's measured "compute" schedule)."""
+    bracketed by CUDA events (the baseline's measured "compute" schedule). It runs for at least
+    ``min_s`` seconds: a sub-second burst would be timed at boost clocks the minutes-long MBS run under
+    the power cap does not see."""
     from paper_2110_12484_b200.losses import compute_loss
     from paper_2110_12484_b200.workloads import build_model, synthetic_data
     torch.manual_seed(0)
@@ -750,6 +757,13 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True
             print(f"no-stream baseline: graph capture failed ({type(e).__name__}: {e}); eager", file=sys.stderr)
     torch.cuda.synchronize(dev)
     n = steps * max(1, min(w.mini, 1024) // batch)
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for i in range(3):
+        one(i)
+    c1.record()
+    torch.cuda.synchronize(dev)
+    n = max(n, int(math.ceil(min_s / (c0.elapsed_time(c1) / 3e3))))
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
     evs[0].record()
     for i in range(n):
