@@ -590,6 +590,9 @@ def run_gpu(args, w, ws, rank, local):
                     "d2h_bytes_per_step": 8 * (4 + 2 * plan.n_s_mu), "ms_per_step": ms_host / e2e_steps,
                     "steps": e2e_steps, "wall_s": wall_host},
             "e2e_vs_no_stream": e2e / nos["value"] if nos else None,
+            # both runs sit at the power cap; their median SM clocks differ by a few % (U-Net: MBS 1492 vs
+            # no-stream 1597 MHz), so the ratio per clock is stated beside the raw one
+            "e2e_vs_no_stream_per_clock": _per_clock(e2e, clocks_e2e.summary(), nos),
             "value_vs_no_stream": value / nos["value"] if nos else None,
             "h2d_overlap_pct": (overhead or {}).get("h2d_overlap_pct"),
             "h2d_overlap_pct_streamer": 100.0 * (1.0 - blocked_ms / copy_ms) if copy_ms > 0 else None,
@@ -688,6 +691,15 @@ def fp32_context(w, dev, n_mu, mini, model_ops, x_dev, y_dev):
 
 
 NO_STREAM_MIN_S = 30.0          # the no-stream baseline runs at least this long (same power / clock state as MBS)
+
+
+def _per_clock(e2e, e2e_clocks: dict, nos: dict | None):
+    """(e2e / its median SM MHz) / (no-stream / its median SM MHz), or None when a clock is missing."""
+    try:
+        a, b = float(e2e_clocks["sm_mhz"]), float(nos["clocks"]["sm_mhz"])
+        return (e2e / a) / (nos["value"] / b)
+    except (TypeError, KeyError, ValueError, ZeroDivisionError):
+        return None
 
 
 def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True, min_s=NO_STREAM_MIN_S):
