@@ -508,11 +508,166 @@ k_stage_nhwc_flat(const uint8_t* __restrict__ src, const int64_t* __restrict__ r
     if (tid == 0) bulk_wait_all();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Warp-specialised NCHW u8 -> NHWC (default). Same balanced split of the flattened pixel space as
+// k_stage_nhwc_flat, but no CTA-wide barrier in the loop (ncu on the flat kernel: 41 % of the warp
+// cycles stalled at __syncthreads behind the one thread that issued loads and the tile store, and
+// 3.75 issued instructions per staged byte):
+//   * warp NCW (the producer) — one lane walks the CTA's pixels with a running (row, offset), no
+//     division per tile, and issues each tile's planes as 1-D bulk copies into a kWsStages-deep ring
+//     (full[s]: transaction bytes; empty[s]: one arrival per consumer warp);
+//   * warps 0..NCW-1 (consumers) — warp w owns the 32*PX-pixel slice w of every tile: it converts its
+//     slice into its own double-buffered NHWC buffer, releases the stage, and its lane 0 sends the slice
+//     out with its own bulk store. Warps run independently; only the ring couples them.
+// u8 -> float is PRMT (byte under the exponent of 2^23, immediate selector, the magic in one register)
+// + one packed FADD2 per two elements; bf16 keeps the upper half-words (one PRMT per two outputs).
+// ---------------------------------------------------------------------------------------------
+constexpr int kWsStages = 4;
+
+template <uint32_t SEL>
+__device__ __forceinline__ uint32_t prmt_sel(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "n"(SEL));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t u8_under_exp(uint32_t w, uint32_t magic, int b) {   // 0x4B0000vv
+    switch (b & 3) {                                     // b is a compile-time constant after unrolling
+        case 0: return prmt_sel<0x7440>(w, magic);
+        case 1: return prmt_sel<0x7441>(w, magic);
+        case 2: return prmt_sel<0x7442>(w, magic);
+        default: return prmt_sel<0x7443>(w, magic);
+    }
+}
+
+__device__ __forceinline__ void sub_2p23_x2(uint32_t& a, uint32_t& b) {   // (a, b) -= 2^23, exact, one FADD2
+    uint64_t v;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "r"(a), "r"(b));
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(v) : "l"(0xCB000000CB000000ull));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(a), "=r"(b) : "l"(v));
+}
+
+template <int C, typename TO>
+constexpr size_t ws_smem_bytes(int px, int ncw) {
+    return (size_t)kWsStages * C * ncw * 32 * px + (size_t)ncw * 2 * 32 * px * C * sizeof(TO);
+}
+
+template <int OUT, int C, int PX, int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32)
+k_stage_nhwc_ws(const uint8_t* __restrict__ src, const int64_t* __restrict__ rows, int64_t row0, int64_t HW,
+                int64_t total_px, int64_t per_cta, typename Out<OUT>::T* __restrict__ dst) {
+    using TO = typename Out<OUT>::T;
+    constexpr int WP = 32 * PX, TP = NCW * WP, E = PX * C;   // px per warp slice, px per tile, outputs per lane
+    static_assert(PX == 8 || PX == 16, "8 or 16 pixels per lane");
+    static_assert(OUT != MBS_F16, "f16 output takes the flat kernel");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[kWsStages], empty[kWsStages];
+    uint8_t* in = smem_raw;                                                        // [S][C][TP]
+    TO* out = reinterpret_cast<TO*>(smem_raw + (size_t)kWsStages * C * TP);       // [NCW][2][WP*C]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t begin = (int64_t)blockIdx.x * per_cta;
+    const int64_t end = min(total_px, begin + per_cta);
+    const int64_t n_mine = end > begin ? (end - begin + TP - 1) / TP : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kWsStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        mbar_init_fence();
+    }
+    __syncthreads();
+
+    if (warp == NCW) {                                    // producer
+        if (lane != 0) return;
+        int64_t r = begin / HW, off = begin - r * HW;
+        int64_t srow = r < total_px / HW ? src_row(rows, row0, r) : 0;
+        for (int64_t i = 0; i < n_mine; ++i) {
+            const int s = (int)(i % kWsStages);
+            if (i >= kWsStages) mbar_wait(&empty[s], (uint32_t)(((i / kWsStages) + 1) & 1));
+            const int npx = (int)min((int64_t)TP, end - (begin + i * TP));
+            mbar_expect_tx(&full[s], (uint32_t)(C * npx));
+            for (int done = 0; done < npx;) {             // one bulk copy per plane per row segment
+                const int seg = (int)min((int64_t)(npx - done), HW - off);
+                const uint8_t* base = src + srow * (int64_t)C * HW + off;
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    bulk_load(in + ((size_t)s * C + c) * TP + done, base + c * HW, (uint32_t)seg, &full[s]);
+                done += seg;
+                off += seg;
+                if (off == HW) {
+                    off = 0;
+                    ++r;
+                    if (r * HW < end) srow = src_row(rows, row0, r);
+                }
+            }
+        }
+        return;
+    }
+
+    const uint32_t magic = 0x4B000000u;
+    const int q0 = warp * WP + lane * PX;                 // this lane's first pixel within a tile
+    for (int64_t i = 0; i < n_mine; ++i) {
+        const int s = (int)(i % kWsStages);
+        const int64_t p0 = begin + i * TP;
+        const int npx = (int)min((int64_t)TP, end - p0);
+        const int wn = min(WP, npx - warp * WP);          // pixels of this warp's slice (<= 0: none)
+        TO* o = out + ((size_t)warp * 2 + (size_t)(i & 1)) * WP * C;
+        if (lane == 0) bulk_wait_read<1>();               // this warp's store of tile i-2 has left o
+        __syncwarp();
+        mbar_wait(&full[s], (uint32_t)((i / kWsStages) & 1));
+        const uint8_t* pl = in + (size_t)s * C * TP;
+        const bool mine = q0 + PX <= npx;                 // npx is a multiple of 16: whole lanes only
+        uint32_t w[C][PX / 4];
+        if (mine) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                if constexpr (PX == 16) {
+                    const uint4 q = *reinterpret_cast<const uint4*>(pl + c * TP + q0);
+                    w[c][0] = q.x; w[c][1] = q.y; w[c][2] = q.z; w[c][3] = q.w;
+                } else {
+                    const uint2 q = *reinterpret_cast<const uint2*>(pl + c * TP + q0);
+                    w[c][0] = q.x; w[c][1] = q.y;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);            // this warp is done reading stage s
+        if (mine) {
+            uint32_t f[E];                                // NHWC order: element k = pixel k / C, channel k % C
+#pragma unroll
+            for (int k = 0; k < E; ++k) f[k] = u8_under_exp(w[k % C][(k / C) >> 2], magic, (k / C) & 3);
+#pragma unroll
+            for (int k = 0; k < E; k += 2) sub_2p23_x2(f[k], f[k + 1]);
+            uint4* d16 = reinterpret_cast<uint4*>(o + (size_t)(lane * PX) * C);
+            if constexpr (OUT == MBS_BF16) {
+#pragma unroll
+                for (int v = 0; v < E / 8; ++v)
+                    d16[v] = make_uint4(prmt_sel<0x7632>(f[8 * v], f[8 * v + 1]), prmt_sel<0x7632>(f[8 * v + 2], f[8 * v + 3]),
+                                        prmt_sel<0x7632>(f[8 * v + 4], f[8 * v + 5]), prmt_sel<0x7632>(f[8 * v + 6], f[8 * v + 7]));
+            } else {
+#pragma unroll
+                for (int v = 0; v < E / 4; ++v) d16[v] = make_uint4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]);
+            }
+        }
+        fence_proxy_async_smem();                         // generic-proxy smem writes -> the bulk store
+        __syncwarp();
+        if (lane == 0 && wn > 0) bulk_store(dst + (p0 + warp * WP) * C, o, (uint32_t)(wn * C * sizeof(TO)));
+    }
+    if (lane == 0) bulk_wait_all();
+}
+
 static int stage_path() {
     // A/B only: 0 = per-row, 1 = grid-stride vec, 2 = smem, 3 = bulk-async per row, 4 = bulk-async over the
-    // flattened, evenly split pixel space (default)
+    // flattened, evenly split pixel space (default), 5 = the same split, warp-specialised (measured slower:
+    // 12.3 vs 11.7 us per C2 micro-batch, profiles/r02_k2_ws_ab.txt)
     const char* e = getenv("MBS_K2_PATH");
     return e ? atoi(e) : 4;
+}
+
+static int ws_px() {   // A/B only: MBS_K2_WS_PX=16 -> 16 pixels per lane (4096-pixel tiles)
+    const char* e = getenv("MBS_K2_WS_PX");
+    return (e && atoi(e) == 16) ? 16 : 8;
 }
 
 static bool flat_small() {   // A/B only: MBS_K2_FLAT=128 -> 128-thread CTAs on 1024-pixel tiles (more CTAs per SM)
@@ -586,6 +741,30 @@ static int launch_flat(const uint8_t* s, const int64_t* rows, int64_t row0, int6
     return MBS_OK;
 }
 
+template <int OUT, int C, int PX, int NCW = 8>
+static int launch_ws(const uint8_t* s, const int64_t* rows, int64_t row0, int64_t n_rows, int64_t HW,
+                     typename Out<OUT>::T* d, cudaStream_t st) {
+    using TO = typename Out<OUT>::T;
+    auto kern = k_stage_nhwc_ws<OUT, C, PX, NCW>;
+    constexpr int NT = (NCW + 1) * 32;
+    constexpr size_t sm = ws_smem_bytes<C, TO>(PX, NCW);
+    static int per_sm = 0;
+    if (!per_sm) {
+        MBS_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        MBS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
+        if (per_sm < 1) per_sm = 1;
+    }
+    const int64_t total = n_rows * HW;
+    static const int cap = getenv("MBS_K2_CTAS_PER_SM") ? atoi(getenv("MBS_K2_CTAS_PER_SM")) : 0;  // A/B only
+    const int64_t resident = (int64_t)sm_count() * (cap > 0 ? std::min(cap, per_sm) : per_sm);
+    int64_t per_cta = (total + resident - 1) / resident;
+    per_cta = std::max<int64_t>(16, (per_cta + 15) / 16 * 16);   // 16-byte aligned bulk copies
+    const int grid = (int)((total + per_cta - 1) / per_cta);
+    kern<<<grid, NT, sm, st>>>(s, rows, row0, HW, total, per_cta, d);
+    MBS_CK_LAUNCH("k_stage_nhwc_ws");
+    return MBS_OK;
+}
+
 static int resident_grid(int64_t units) {
     static int sms = 0;
     if (!sms) {
@@ -636,7 +815,21 @@ static int stage_typed(const void* src, const int64_t* rows, int64_t row0, int64
                               (da % 16 == 0) && ((kPix * sizeof(TO)) % 16 == 0);
         const int path = stage_path();
         if constexpr (sizeof(TI) == 1) {
-            if (path == 4 && nhwc && C <= 4 && HW % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
+            if (path == 5 && OUT != MBS_F16 && nhwc && C <= 4 && HW % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
+                is_device_memory(src)) {
+                if constexpr (OUT != MBS_F16) {
+                    const bool wide = ws_px() == 16;
+                    switch (C) {
+                        case 2: return wide ? launch_ws<OUT, 2, 16>(s, rows, row0, n_rows, HW, d, st)
+                                            : launch_ws<OUT, 2, 8>(s, rows, row0, n_rows, HW, d, st);
+                        case 3: return wide ? launch_ws<OUT, 3, 16>(s, rows, row0, n_rows, HW, d, st)
+                                            : launch_ws<OUT, 3, 8>(s, rows, row0, n_rows, HW, d, st);
+                        default: return wide ? launch_ws<OUT, 4, 16>(s, rows, row0, n_rows, HW, d, st)
+                                             : launch_ws<OUT, 4, 8>(s, rows, row0, n_rows, HW, d, st);
+                    }
+                }
+            }
+            if ((path == 4 || path == 5) && nhwc && C <= 4 && HW % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
                 is_device_memory(src)) {
                 switch (C) {
                     case 2: return launch_flat<OUT, 2, 2048>(s, rows, row0, n_rows, HW, d, st);
@@ -658,7 +851,7 @@ static int stage_typed(const void* src, const int64_t* rows, int64_t row0, int64
                 }
             }
         }
-        if ((path == 2 || path == 3 || path == 4) && nhwc && C <= 4 && (HW * (int64_t)sizeof(TI)) % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
+        if ((path >= 2 && path <= 5) && nhwc && C <= 4 && (HW * (int64_t)sizeof(TI)) % 16 == 0 && sa % 16 == 0 && da % 16 == 0 &&
             ((int64_t)kTilePx * C * sizeof(TO)) % 16 == 0 && (HW * C * (int64_t)sizeof(TO)) % 16 == 0) {
             const int64_t tpr = (HW + kTilePx - 1) / kTilePx, total = n_rows * tpr;
             const size_t sm = (size_t)kTilePx * C * sizeof(TO);

@@ -56,18 +56,20 @@ def test_stage_bit_exact(cuda, src_dtype, dst_dtype, shape, cl):
     assert torch.equal(_bits(got2), _bits(want2))
 
 
-@pytest.mark.parametrize("path", ["0", "1", "2", "3", "3:2048", "4", "4:flat128"])
+@pytest.mark.parametrize("path", ["0", "1", "2", "3", "3:2048", "4", "4:flat128", "5", "5:ws16"])
 @pytest.mark.parametrize("dst_dtype", [torch.float32, torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("shape", [(9, 3, 80, 80), (5, 3, 224, 224), (7, 4, 64, 64), (6, 2, 48, 48),
                                    (300, 3, 16, 16)])
 def test_stage_u8_nhwc_every_path(cuda, monkeypatch, path, dst_dtype, shape):
     """Every K2 NHWC implementation (MBS_K2_PATH: per-row, grid-stride, smem tile, bulk-async TMA ring per row,
-    bulk-async over the flattened pixel space with tiles crossing rows) is
+    bulk-async over the flattened pixel space with tiles crossing rows, its warp-specialised form with 8 or 16
+    pixels per lane) is
     bit-exact, including ragged last tiles (80x80 = 4096 + 2304 px, 224x224 = 12 x 4096 + 1024 px) and
     more tiles than resident CTAs."""
     monkeypatch.setenv("MBS_K2_PATH", path.split(":")[0])
     monkeypatch.setenv("MBS_K2_TILE", path.split(":")[-1])
     monkeypatch.setenv("MBS_K2_FLAT", "128" if path.endswith("flat128") else "0")
+    monkeypatch.setenv("MBS_K2_WS_PX", "16" if path.endswith("ws16") else "8")
     x = _src(torch.uint8, shape, cuda)
     rows = torch.from_numpy(O.epoch_order(shape[0], 5, 2).astype(np.int64)).to(cuda)
     st = Staging(dtype=dst_dtype, channels_last=True)
