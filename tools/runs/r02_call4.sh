@@ -25,6 +25,6 @@ timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --cloc
     --log-file gpurun_out/c4_default.csv python tools/profile_step.py > /dev/null 2>&1
 MBS_NATIVE_LIB=$PWD/ab/libmbs_k1u4.so timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none -k regex:"k_stage|k_accum" -c 8 --csv \
     --log-file gpurun_out/c4_u4.csv python tools/profile_step.py > /dev/null 2>&1
-bash tools/r02_sanitize_k1c.sh
+bash tools/runs/r02_sanitize_k1c.sh
 MBS_PARITY_REPORT=$PWD/gpurun_out/parity_report.jsonl timeout 1200 python -m pytest tests/test_bench_stack_parity_gpu.py -q -m gpu -p no:cacheprovider > gpurun_out/c4_parity.log 2>&1; tail -3 gpurun_out/c4_parity.log
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/c4_pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/c4_pytest_gpu.log; tail -4 gpurun_out/c4_pytest_gpu.log

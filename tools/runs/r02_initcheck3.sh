@@ -11,4 +11,4 @@ for grp in K S; do
   grep -h -A2 "Uninitialized" gpurun_out/san_init3_${grp}.log | grep " at " | sort | uniq -c | head -5 >> gpurun_out/san_init3_summary.txt
 done
 cat gpurun_out/san_init3_summary.txt
-bash tools/r02_k2_ab.sh
+bash tools/runs/r02_k2_ab.sh
