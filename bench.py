@@ -463,7 +463,11 @@ def run_gpu(args, w, ws, rank, local):
         while b >= 1 and r is None:
             try:
                 with ClockSampler(dev.index) as ck:
-                    r = no_stream_baseline(w, dev, b, args.steps, args.warmup, ws, ops=ops_)
+                    # the same-model baseline runs as long as the timed e2e run (its power / clock state: a
+                    # 30 s U-Net@384 run held 1,597 MHz against the 206 s MBS run's 1,492 under the power cap)
+                    min_s = NO_STREAM_MIN_S if ops_ != args.model_ops else \
+                        min(NO_STREAM_MAX_S, max(NO_STREAM_MIN_S, ms_host / 1e3))
+                    r = no_stream_baseline(w, dev, b, args.steps, args.warmup, ws, ops=ops_, min_s=min_s)
                 r["clocks"] = ck.summary()
             except torch.OutOfMemoryError:
                 b //= 2
@@ -691,6 +695,7 @@ def fp32_context(w, dev, n_mu, mini, model_ops, x_dev, y_dev):
 
 
 NO_STREAM_MIN_S = 30.0          # the no-stream baseline runs at least this long (same power / clock state as MBS)
+NO_STREAM_MAX_S = 300.0         # ... and as long as the timed e2e run, up to this
 
 
 def _per_clock(e2e, e2e_clocks: dict, nos: dict | None):
