@@ -15,7 +15,9 @@ optimizer step. ``--config c2`` is the fits-in-HBM 1024/128 case.
 * ``e2e``     — the same API fed from PINNED HOST memory: every micro-batch is copied H2D through the
   streamer inside the timed region and every mini-batch's loss is read back (D2H).
 * ``no_stream`` — plain torch training at batch = micro, data resident (the paper's "w/o MBS" run);
-  ``e2e_vs_no_stream`` is the north-star ratio.
+  ``e2e_vs_no_stream`` is the north-star ratio; ``no_stream_weights_at_init`` is the same run with the
+  weights held at init (lr 1e-9), the matched-power-state baseline (the weight trajectory, not MBS,
+  sets the power-capped clock on synthetic data: profiles/r02_power_state.md).
 * ``overhead`` — the reference's overhead report (streaming.py:130-149) on the MEASURED schedule of
   the timed e2e run (``streaming.ScheduleTracer``: CUDA events per micro-batch on the copy and
   compute streams), and the H2D overlap fraction from the same events.
@@ -467,7 +469,8 @@ def run_gpu(args, w, ws, rank, local):
                     # 30 s U-Net@384 run held 1,597 MHz against the 206 s MBS run's 1,492 under the power cap)
                     min_s = NO_STREAM_MIN_S if ops_ != args.model_ops else \
                         min(NO_STREAM_MAX_S, max(NO_STREAM_MIN_S, ms_host / 1e3))
-                    r = no_stream_baseline(w, dev, b, args.steps, args.warmup, ws, ops=ops_, min_s=min_s)
+                    r = no_stream_baseline(w, dev, b, args.steps, args.warmup, ws, ops=ops_, min_s=min_s,
+                                           data=(x_dev, y_dev))
                 r["clocks"] = ck.summary()
             except torch.OutOfMemoryError:
                 b //= 2
@@ -476,6 +479,20 @@ def run_gpu(args, w, ws, rank, local):
             nos = r
         else:
             nos_torch = r
+    # the same baseline with the weights held at init (lr 1e-9): the MBS run takes one optimizer step per
+    # mini-batch, the baseline one per micro-batch, and on synthetic data the power a step draws depends on
+    # the weight state — U-Net@384: the MBS engine at one micro per step runs 1,717 MHz / 1,289 samples/s
+    # at lr 0.01 and 1,500 MHz / 1,165 at lr 1e-9, all at the 985 W cap (profiles/r02_power_state.md)
+    nos_init = None
+    if nos is not None:
+        try:
+            with ClockSampler(dev.index) as ck:
+                nos_init = no_stream_baseline(w, dev, nos["batch"], args.steps, args.warmup, ws, ops=args.model_ops,
+                                              data=(x_dev, y_dev), lr=1e-9)
+            nos_init["clocks"] = ck.summary()
+        except torch.OutOfMemoryError:
+            nos_init = None
+        torch.cuda.empty_cache()
 
     # --- the reference's overhead report on the measured schedules ---
     overhead = None
@@ -597,12 +614,14 @@ def run_gpu(args, w, ws, rank, local):
             # both runs sit at the power cap; their median SM clocks differ by a few % (U-Net: MBS 1492 vs
             # no-stream 1597 MHz), so the ratio per clock is stated beside the raw one
             "e2e_vs_no_stream_per_clock": _per_clock(e2e, clocks_e2e.summary(), nos),
+            "e2e_vs_no_stream_weights_at_init": e2e / nos_init["value"] if nos_init else None,
             "value_vs_no_stream": value / nos["value"] if nos else None,
             "h2d_overlap_pct": (overhead or {}).get("h2d_overlap_pct"),
             "h2d_overlap_pct_streamer": 100.0 * (1.0 - blocked_ms / copy_ms) if copy_ms > 0 else None,
             "h2d_gbs": h2d_gbs, "accum_gbs": k1.get("gbs"),
             "no_stream": {k: v for k, v in (nos or {}).items() if k != "events"} or None,
             "no_stream_torch_ops": {k: v for k, v in (nos_torch or {}).items() if k != "events"} or None,
+            "no_stream_weights_at_init": {k: v for k, v in (nos_init or {}).items() if k != "events"} or None,
             "overhead": overhead, "roofline": roofline, "roofline_k5": roofline_k5, "model_flops": model_flops,
             "precision": precision, "precision_fp32": fp32_ctx,
             "gpu_launches": launches_value, "gpu_launches_e2e": launches_e2e,
@@ -696,6 +715,7 @@ def fp32_context(w, dev, n_mu, mini, model_ops, x_dev, y_dev):
 
 NO_STREAM_MIN_S = 30.0          # the no-stream baseline runs at least this long (same power / clock state as MBS)
 NO_STREAM_MAX_S = 300.0         # ... and as long as the timed e2e run, up to this
+NO_STREAM_POOL = 64             # distinct batches the baseline cycles through
 
 
 def _per_clock(e2e, e2e_clocks: dict, nos: dict | None):
@@ -707,7 +727,8 @@ def _per_clock(e2e, e2e_clocks: dict, nos: dict | None):
         return None
 
 
-def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True, min_s=NO_STREAM_MIN_S):
+def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True, min_s=NO_STREAM_MIN_S, data=None,
+                       lr=0.01):
     """The paper's 'w/o MBS' run: plain torch training, batch = micro-batch, data resident in HBM.
 
     ``ops`` selects the same model definition as the MBS run (native K5/K6/K7 or stock torch ops).
@@ -716,20 +737,29 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True
     tracks the host CPU rather than the GPU. Falls back to eager if capture fails. Every step is
     bracketed by CUDA events (the baseline's measured "compute" schedule). It runs for at least
     ``min_s`` seconds: a sub-second burst would be timed at boost clocks the minutes-long MBS run under
-    the power cap does not see."""
+    the power cap does not see. ``lr``: 0.01 is the run's own learning rate; 1e-9 keeps the weights at
+    their initial values (the matched-weight-state run, see bench's ``no_stream_weights_at_init``). ``data``: the MBS run's own (HBM-resident) dataset; the baseline then cycles
+    through its first NO_STREAM_POOL batches (pre-staged to bf16 NHWC, untimed) instead of two synthetic
+    ones, so both runs train on data of the same statistics (two repeated batches are memorised within
+    seconds; the shrinking gradients then lower the power draw and flatter the baseline's clock)."""
     from paper_2110_12484_b200.losses import compute_loss
     from paper_2110_12484_b200.workloads import build_model, synthetic_data
     torch.manual_seed(0)
     model = build_model(w, ops=ops).to(dev).to(memory_format=torch.channels_last)
     if w.optimizer == "sgd":
-        opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9, weight_decay=5e-4, fused=True)
+        opt = torch.optim.SGD(model.parameters(), lr=lr, momentum=0.9, weight_decay=5e-4, fused=True)
     else:
-        opt = torch.optim.Adam(model.parameters(), lr=0.01, weight_decay=5e-4, fused=True, capturable=graph)
-    x, y = synthetic_data(w, 2 * batch, seed=7, device=dev)
-    y = y.float() if y.dtype == torch.uint8 else y
+        opt = torch.optim.Adam(model.parameters(), lr=lr, weight_decay=5e-4, fused=True, capturable=graph)
+    if data is not None and data[0].shape[0] >= 2 * batch:
+        x, y = data
+        n_pool = min(NO_STREAM_POOL, x.shape[0] // batch)
+    else:
+        x, y = synthetic_data(w, 2 * batch, seed=7, device=dev)
+        n_pool = 2
     xs = [x[i * batch:(i + 1) * batch].to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
-          for i in range(2)]
-    ys = [y[i * batch:(i + 1) * batch] for i in range(2)]
+          for i in range(n_pool)]
+    ys = [y[i * batch:(i + 1) * batch] for i in range(n_pool)]
+    ys = [t.float() if t.dtype == torch.uint8 else t for t in ys]
     sx, sy = xs[0].clone(), ys[0].clone()
 
     def step(cache=True):
@@ -740,8 +770,8 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True
         return loss
 
     def one(i):
-        sx.copy_(xs[i % 2])
-        sy.copy_(ys[i % 2])
+        sx.copy_(xs[i % n_pool])
+        sy.copy_(ys[i % n_pool])
         step()
         opt.zero_grad(set_to_none=True)
 
@@ -764,8 +794,8 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True
                 step(cache=False)
 
             def one(i):                                  # noqa: F811 - the graphed step
-                sx.copy_(xs[i % 2])
-                sy.copy_(ys[i % 2])
+                sx.copy_(xs[i % n_pool])
+                sy.copy_(ys[i % n_pool])
                 g.replay()
             for i in range(2):
                 one(i)
@@ -792,7 +822,9 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True
               for i in range(n)]
     del model, opt
     return {"value": batch * n * ws / (ms / 1e3), "unit": "samples/s", "batch": batch, "steps": n,
-            "samples": batch * n, "model_ops": ops, "how": how, "events": events}
+            "samples": batch * n, "model_ops": ops, "how": how, "events": events,
+            "data": (f"the first {n_pool} batches ({n_pool * batch} samples) of the MBS run's dataset, cycled"
+                     if n_pool > 2 else "two synthetic batches, cycled")}
 
 
 if __name__ == "__main__":
