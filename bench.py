@@ -520,6 +520,13 @@ def run_gpu(args, w, ws, rank, local):
                            "baseline = the no-stream run's measured per-sample time x N_B (it ran "
                            f"{nos['samples'] if nos else 0} samples); overlap = 1 - (compute-stream wait on "
                            "copies) / (copy time), from the same events"}
+        if nos_init:
+            base_mk = n_b / (nos_init["value"] / ws)
+            rep0 = SS.overhead_report(mbs_sched, SS.StreamSchedule(
+                tuple(SS.StreamEvent(*e) for e in nos_init["events"]), base_mk, False))
+            overhead["vs_weights_at_init"] = {"no_stream_makespan_s": rep0.baseline_makespan,
+                                              "overhead_pct": rep0.overhead_pct,
+                                              "overhead_seconds": rep0.overhead_seconds}
 
     k1 = kstats.get("k1_accumulate", {})
     peak, peak_kind = _peaks()
