@@ -587,7 +587,12 @@ def run_gpu(args, w, ws, rank, local):
     fp32_ctx = None
     if not args.no_fp32_context and ws == 1:
         _graphs.clear()
-        fp32_ctx = fp32_context(w, dev, n_mu, warm_small, args.model_ops, x_dev, y_dev)
+        torch.cuda.empty_cache()
+        try:
+            fp32_ctx = fp32_context(w, dev, n_mu, warm_small, args.model_ops, x_dev, y_dev)
+        except torch.OutOfMemoryError as e:                # context only: never lose the line to it
+            fp32_ctx = {"unavailable": f"OutOfMemoryError: {str(e)[:120]}"}
+        torch.cuda.empty_cache()
 
     config = workload_config(w, n_b, n_mu, ws)
     setup = {"model": w.model,
@@ -723,6 +728,7 @@ def fp32_context(w, dev, n_mu, mini, model_ops, x_dev, y_dev):
 NO_STREAM_MIN_S = 30.0          # the no-stream baseline runs at least this long (same power / clock state as MBS)
 NO_STREAM_MAX_S = 300.0         # ... and as long as the timed e2e run, up to this
 NO_STREAM_POOL = 64             # distinct batches the baseline cycles through
+NO_STREAM_POOL_BYTES = 2 << 30  # ... within this many staged bytes (C5's auto-sized micro-batch leaves no room)
 
 
 def _per_clock(e2e, e2e_clocks: dict, nos: dict | None):
@@ -759,7 +765,8 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True
         opt = torch.optim.Adam(model.parameters(), lr=lr, weight_decay=5e-4, fused=True, capturable=graph)
     if data is not None and data[0].shape[0] >= 2 * batch:
         x, y = data
-        n_pool = min(NO_STREAM_POOL, x.shape[0] // batch)
+        staged = batch * (x[0].numel() * 2 + (y[0].numel() * 4 if y.dim() > 1 else 8))   # bf16 image + target
+        n_pool = max(2, min(NO_STREAM_POOL, x.shape[0] // batch, NO_STREAM_POOL_BYTES // staged))
     else:
         x, y = synthetic_data(w, 2 * batch, seed=7, device=dev)
         n_pool = 2
@@ -831,7 +838,7 @@ def no_stream_baseline(w, dev, batch, steps, warmup, ws, ops="torch", graph=True
     return {"value": batch * n * ws / (ms / 1e3), "unit": "samples/s", "batch": batch, "steps": n,
             "samples": batch * n, "model_ops": ops, "how": how, "events": events,
             "data": (f"the first {n_pool} batches ({n_pool * batch} samples) of the MBS run's dataset, cycled"
-                     if n_pool > 2 else "two synthetic batches, cycled")}
+                     if data is not None and data[0].shape[0] >= 2 * batch else "two synthetic batches, cycled")}
 
 
 if __name__ == "__main__":
