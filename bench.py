@@ -458,6 +458,7 @@ def run_gpu(args, w, ws, rank, local):
 
     # --- no-stream baseline: plain torch training at batch = micro, data resident ---
     _graphs.clear()
+    torch.cuda.empty_cache()             # the MBS graphs' pools back to the driver (C5 fills HBM by design)
     nos = nos_torch = None
     for ops_ in (args.model_ops, "torch") if args.model_ops != "torch" else (args.model_ops,):
         b = n_mu
